@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the resampling hot path (driver contract).
+
+Default workload (BASELINE.json "metric", config 3): dac_sampler at
+M = 2^26 heavy-tailed weights (log w ~ N(0, 4^2), seed 1003), N = 2^16 draws
+(stream seed 2003).  A step is one sampler call: sorted uniforms + search,
+with the table already built and resident (the reference's timed region,
+bench.py:193-204).  Metric = algorithmic bytes (8M + 16N) / step time, plus
+samples/s.  L2 is flushed (256 MiB write) before every timed step; steps
+are timed one by one with CUDA events on the launching stream.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
+                  [--sampler dac|ccf|binary] [--mode auto|merge|search]
+                  [--impl drs|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle's C port of the numba kernels + numpy pipeline, pinned bit-exact to
+the reference) on this host's cores, same config and metric.
+Under torchrun every rank runs an independent replica of the single-GPU
+workload (weak scaling) except config c5, which shards one M = 2^30 table
+over the ranks (one 24-byte-per-rank all-gather) and config c4, which
+shards the 4096 filters by rank.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": dict(M=1 << 16, N=1 << 10, sigma=1.0, wseed=1001, useed=2001),
+    "c2": dict(M=1 << 20, N=1 << 20, sigma=1.0, wseed=1002, useed=2002),
+    "c3": dict(M=1 << 26, N=1 << 16, sigma=4.0, wseed=1003, useed=2003),
+    "c4": dict(B=4096, Mf=16384, Nf=256, wseed=1004, useed=2004),
+    "c5": dict(M=1 << 30, N=1 << 24, sigma=2.0, wseed=1005, useed=2005),
+}
+METRIC = "weights-scanned GB/s (frac of HBM peak) + samples/sec, M=2^26 N=2^16"
+
+
+def peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------ inputs
+def make_weights(cfg_name, rank=0, world=1):
+    c = CONFIGS[cfg_name]
+    if cfg_name == "c4":
+        rng = np.random.default_rng(c["wseed"])
+        B, Mf = c["B"], c["Mf"]
+        lo, hi = B * rank // world, B * (rank + 1) // world
+        pi = rng.dirichlet(np.ones(64), size=B)[lo:hi]
+        out = np.empty((hi - lo, Mf))
+        for b in range(hi - lo):  # chi-square field per filter, row-major (n, p)
+            frng = np.random.default_rng([c["wseed"], lo + b])
+            q = frng.chisquare(6, size=(256, 64))
+            out[b] = np.exp(np.log(1 / 256) + np.log(pi[b])[None, :] - 0.5 * q).reshape(Mf)
+        return out
+    M = c["M"]
+    if cfg_name == "c5":
+        a, b = M * rank // world, M * (rank + 1) // world
+        # 64 chunks of 2^24 from per-chunk generators; spike block holds 25% of the mass
+        chunk = 1 << 24
+        w = np.empty(b - a)
+        for k in range(a // chunk, (b + chunk - 1) // chunk):
+            g = np.exp(2.0 * np.random.default_rng([c["wseed"], k]).standard_normal(chunk))
+            s0, s1 = max(a, k * chunk), min(b, (k + 1) * chunk)
+            w[s0 - a:s1 - a] = g[s0 - k * chunk:s1 - k * chunk]
+        off = int(np.random.default_rng([c["wseed"], 999]).integers(0, M - 1024))
+        # expected total mass of the log-normal field is M e^2; the block gets a third of it
+        spike = M * np.exp(2.0) / 3.0 / 1024
+        lo, hi = max(a, off), min(b, off + 1024)
+        if lo < hi:
+            w[lo - a:hi - a] = spike
+        return w
+    rng = np.random.default_rng(c["wseed"])
+    return np.exp(c["sigma"] * rng.standard_normal(M))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                   capture_output=True, text=True, timeout=5)
+                if r.returncode == 0 and r.stdout.strip():
+                    self.rows.append([x.strip() for x in r.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > i + 2 and r[i + 2] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- drs arm
+def run_drs(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_01356_b200 as drs
+    from paper_2604_01356_b200 import _lib
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    cfg = args.config
+    c = CONFIGS[cfg]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def l2_flush():
+        flush.fill_(1)
+
+    # ---- untimed setup (the reference builds its table untimed too)
+    if cfg == "c4":
+        w_host = make_weights(cfg, rank, world)
+        w = torch.from_numpy(w_host).to(dev)
+        B, Mf, Nf = w.shape[0], c["Mf"], c["Nf"]
+        streams = [drs.RngStream(c["useed"], (rank * 100000 + b,)) for b in range(B)]
+        alg_bytes = B * (8 * Mf + 16 * Nf)
+        samples = B * Nf
+
+        def step():
+            keys = drs.batched.stream_keys(streams, Nf)
+            return drs.resample_batched(w, Nf, keys, return_uniforms=True, check=False)
+
+        launches_per_step = 1
+        kernel_step = step
+        e2e_step = lambda: drs.resample_batched(w_host, Nf, streams, return_uniforms=True)  # noqa: E731
+        e2e_h2d, e2e_d2h = 8 * B * Mf + 24 * B, 16 * B * Nf
+    elif cfg == "c5" and world > 1:
+        w_host = make_weights(cfg, rank, world)
+        table = drs.build_sharded_table(torch.from_numpy(w_host).to(dev))
+        N = c["N"]
+        stream = drs.RngStream(c["useed"])
+        alg_bytes = (8 * c["M"]) // world + 16 * N // world
+        samples = N // world
+
+        def step():
+            return drs.sharded_dac_sampler(table, N, stream)
+
+        launches_per_step = 4
+        kernel_step = step
+        e2e_step = None
+        e2e_h2d = e2e_d2h = 0
+    else:
+        w_host = make_weights(cfg)
+        table = drs.build_weight_table(w_host)
+        M, N = c["M"], c["N"]
+        stream = drs.RngStream(c["useed"], (rank,))
+        alg_bytes = 8 * M + 16 * N
+        samples = N
+        sampler = {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}[args.sampler]
+        kw = {"mode": args.mode} if args.sampler == "dac" else {}
+
+        def step():
+            return sampler(table, N, stream, device=True, **kw)
+
+        launches_per_step = 1 if args.sampler == "binary" else 3
+        # the dominant kernel alone: the search over a fixed U
+        U = drs.randkit.sorted_uniforms_device(drs.RngStream(c["useed"], (rank, 7)), N)
+        match = {"dac": lambda: drs.dac_match(U, table, check=False, mode=args.mode),
+                 "ccf": lambda: drs.ccf_match(U, table, check=False),
+                 "binary": lambda: drs.samplers._lower_bounds(table, U)}[args.sampler]
+        kernel_step = match
+        e2e_step = lambda: sampler(table, N, stream, **kw)  # noqa: E731
+        e2e_h2d, e2e_d2h = 0, 8 * N
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        step()
+        kernel_step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: per-step events, L2 flushed before each step
+    s = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            l2_flush()
+            starts[i].record(s)
+            step()
+            ends[i].record(s)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+
+    # ---- dominant kernel alone (live, same flush discipline)
+    k_ms = []
+    for _ in range(args.steps):
+        l2_flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        kernel_step()
+        b.record(s)
+        torch.cuda.synchronize()
+        k_ms.append(a.elapsed_time(b))
+    kernel_ms = statistics.median(k_ms)
+
+    # ---- end to end through the public API, host result (and host weights for c4)
+    e2e = None
+    if e2e_step is not None:
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / args.steps
+        e2e = {"value": world * alg_bytes / e2e_s / 1e9, "unit": "GB/s", "samples_per_s": world * samples / e2e_s,
+               "ms_per_step": 1e3 * e2e_s, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
+               "timer": "host perf_counter around the public call (result copied to host)"}
+
+    value = world * alg_bytes / (ms_per_step * 1e-3) / 1e9
+    peak, peak_src = peak_hbm()
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
+    traffic = None
+    tp = ROOT / "profiles" / f"traffic_{cfg}_{args.sampler}_{args.mode}.json"
+    if tp.exists():
+        traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+    line = {
+        "metric": METRIC if cfg == "c3" else f"weights-scanned GB/s + samples/sec, {cfg}",
+        "value": value,
+        "unit": "GB/s",
+        "samples_per_s": world * samples / (ms_per_step * 1e-3),
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong" if (cfg == "c5" and world > 1) else "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (seeded numpy weights, SURVEY.md 8(d)); Philox draws",
+        "config": {
+            "workload": cfg, **{k: v for k, v in c.items()}, "sampler": args.sampler, "mode": args.mode,
+            "timed": "sorted uniforms + search per step, table resident (reference bench.py:193-204)",
+            "l2": "flushed (256 MiB write) before every timed step; steps timed individually",
+            "parallelism": ("shard-W" if cfg == "c5" else ("shard-filters" if cfg == "c4" else "replicas")) + f"x{world}",
+        },
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel_ms": kernel_ms, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clk.summary(),
+        "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
+    }
+    return line, (alg_bytes, samples)
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(cfg, sampler, seconds=10.0, threads=1):
+    from oracle import oracle as orc
+
+    c = CONFIGS[cfg]
+    if cfg in ("c4", "c5"):
+        cfg = "c3"
+        c = CONFIGS[cfg]
+    w = make_weights(cfg)
+    W, _ = orc.port_build_table(w)
+    M, N = c["M"], c["N"]
+    k0, k1 = orc.key_of(c["useed"])
+    one = orc.port_throughput(sampler, W, N, 1, 1, k0, k1)  # includes first-touch
+    one = orc.port_throughput(sampler, W, N, 1, 1, k0, k1)
+    calls = max(1, int(seconds / max(one, 1e-6) / threads))
+    el = orc.port_throughput(sampler, W, N, threads, calls, k0, k1)
+    per = el / calls  # wall time per call per thread (threads run concurrently)
+    value = threads * (8 * M + 16 * N) / per / 1e9
+    return {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+            "samples_per_s": threads * N / per,
+            "sample": f"{cfg} {sampler}_sampler x{calls * threads} calls ({threads} thread(s)), {el:.1f} s, "
+                      "oracle C port of the reference path (pinned bit-exact to the reference)",
+            "ms_per_call": 1e3 * per}
+
+
+def run_reference(args):
+    threads = os.cpu_count() or 1
+    cb = cpu_baseline(args.config, args.sampler, seconds=max(5.0, min(30.0, 2.0 * args.steps)), threads=threads)
+    line = {
+        "impl": "reference",
+        "metric": METRIC if args.config == "c3" else f"weights-scanned GB/s + samples/sec, {args.config}",
+        "value": cb["value"], "unit": "GB/s", "samples_per_s": cb["samples_per_s"],
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": cb["ms_per_call"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded numpy weights); Philox draws",
+        "config": {"workload": args.config, **CONFIGS[args.config], "sampler": args.sampler},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--sampler", default="dac", choices=["dac", "ccf", "binary"])
+    ap.add_argument("--mode", default="auto", choices=["auto", "merge", "search"])
+    ap.add_argument("--impl", default="drs", choices=["drs", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line, _ = run_drs(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.config, args.sampler, seconds=args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * drs.h -- C ABI of libdrs.so, the B200 (sm_100a) multinomial-resampling
+ * library behind the paper_2604_01356_b200 package.
+ *
+ * Every entry point is extern "C", takes plain device pointers, sizes and a
+ * cudaStream_t passed as void*, never allocates, never synchronises, and is
+ * stream-ordered on the caller's stream.  Scratch comes from a caller-owned
+ * workspace sized by dr_workspace_bytes() and initialised once with
+ * dr_workspace_init().  A workspace serves one stream at a time.
+ *
+ * Return value: 0 on success, a negative DRS_ERR_* on bad arguments or a
+ * launch failure (dr_strerror).  Data-dependent conditions -- the ones the
+ * reference reports as ValueError -- are OR-ed into a device int32 status
+ * word (DRS_ST_* bits) that the caller reads only where the reference would
+ * raise.
+ *
+ * Each function names the reference interface it replaces
+ * (/root/reference/pkg/src/dacresample/<file>:<line>).
+ */
+#ifndef DRS_H
+#define DRS_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* --- geometry of the device scan association --- */
+#define DRS_SCAN_LANES 32
+#define DRS_SCAN_WARPS 8
+#define DRS_SCAN_K_TABLE 33 /* elements per lane chunk, table scans   */
+#define DRS_SCAN_K_UNIF 4   /* elements per lane chunk, spacing scans */
+#define DRS_INDEX_FANOUT 16
+#define DRS_INDEX_MAX_LEVELS 12
+
+/* --- return codes --- */
+#define DRS_OK 0
+#define DRS_ERR_ARG (-1)       /* invalid size / null pointer               */
+#define DRS_ERR_WORKSPACE (-2) /* workspace too small                       */
+#define DRS_ERR_LAUNCH (-3)    /* CUDA launch error (cudaGetLastError)      */
+#define DRS_ERR_ALIGN (-4)     /* pointer not aligned as documented         */
+#define DRS_ERR_MODE (-5)      /* unknown mode                              */
+
+/* --- status bits (device int32) --- */
+#define DRS_ST_INVALID_WEIGHT 0x1   /* cdf.py:74-75  "invalid weight"            */
+#define DRS_ST_DEGENERATE 0x2       /* cdf.py:77-78  "degenerate distribution"   */
+#define DRS_ST_ACCUM_OVERFLOW 0x4   /* cdf.py:83-84  "accumulation overflow"     */
+#define DRS_ST_NOT_SORTED 0x8       /* samplers.py:74-75 "input not sorted"      */
+#define DRS_ST_OUT_OF_SUPPORT 0x10  /* samplers.py:72-73 "uniforms must lie in (0, 1]" */
+#define DRS_ST_REPAIRED 0x20        /* randkit.py:95-100 repair pass taken       */
+#define DRS_ST_NONFINITE 0x40       /* cdf.py:35-36 (WeightTable) "invalid weight" */
+#define DRS_ST_DECREASING 0x80      /* cdf.py:37-38 "non-decreasing from >= 0"   */
+#define DRS_ST_TOP_NOT_ONE 0x100    /* cdf.py:39-40 "must end at exactly 1"      */
+
+/* --- workspace ops for dr_workspace_bytes --- */
+#define DRS_OP_TABLE 1
+#define DRS_OP_SORTED 2
+
+/* --- dac modes --- */
+#define DRS_DAC_AUTO 0   /* merge when M <= tau*N, else index search          */
+#define DRS_DAC_MERGE 1  /* W-tiled merge (reads all of W; north-star recast) */
+#define DRS_DAC_SEARCH 2 /* per-u 16-ary index search                         */
+
+const char *dr_version(void);
+const char *dr_strerror(int code);
+/* writes LANES, WARPS, K_TABLE, K_UNIF, FANOUT into g[0..4] */
+void dr_scan_geometry(int32_t g[5]);
+
+size_t dr_workspace_bytes(int op, int64_t M, int64_t N, int64_t B);
+int dr_workspace_init(void *ws, size_t ws_bytes, void *stream);
+
+/* doubles of the search index for an M-entry table (0 if M <= 16) */
+int64_t dr_index_entries(int64_t M);
+
+/* build_weight_table (cdf.py:59-89): w[M] raw weights -> W[M] cumulative
+ * weights with W[M-1] == 1 exactly, idx[dr_index_entries(M)] search index.
+ * status gets INVALID_WEIGHT / DEGENERATE / ACCUM_OVERFLOW.  W and w must be
+ * 16-byte aligned. */
+int dr_build_table(const double *w, int64_t M, double *W, double *idx, int32_t *status,
+                   void *ws, size_t ws_bytes, void *stream);
+
+/* WeightTable.__init__ validation (cdf.py:31-42) of a caller-supplied
+ * cumulative array: NONFINITE / DECREASING / TOP_NOT_ONE. */
+int dr_validate_table(const double *W, int64_t M, int32_t *status, void *stream);
+
+/* search index of an existing table (what dr_build_table writes as a side product) */
+int dr_build_index(const double *W, int64_t M, double *idx, void *stream);
+
+/* RngStream.uniforms (randkit.py:47-55): k draws of the numpy-Philox4x64-10
+ * stream (key k0,k1) starting at raw draw `offset`, as doubles in (0,1). */
+int dr_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t k, double *u, void *stream);
+
+/* sorted_uniforms (randkit.py:70-101): n+1 draws from `offset` -> spacings
+ * -log u -> chained scan -> U[i] = Z[i]/Z[n], with the exact collapse
+ * repair (randkit.py:104-116).  status gets REPAIRED when it ran. */
+int dr_sorted_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, double *U,
+                       int32_t *status, void *ws, size_t ws_bytes, void *stream);
+
+/* same, with the n+1 underlying uniforms supplied (duck-typed host streams,
+ * e.g. the reference tests' ReplayStream) */
+int dr_sorted_uniforms_from(const double *raw, int64_t n, double *U, int32_t *status,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* _binary_kernel (samplers.py:93-97): out[i] = first j with W[j] >= u[i]
+ * (clamped to M-1), any order of u.  idx from dr_build_table/dr_build_index;
+ * W must be 32-byte aligned. */
+int dr_match_binary(const double *W, const double *idx, int64_t M, const double *u,
+                    int64_t N, int64_t *out, void *stream);
+
+/* binary_sampler (samplers.py:238-252) fused: draws N uniforms from the
+ * stream at `offset` and searches them, output in draw order. */
+int dr_sample_binary(const double *W, const double *idx, int64_t M, uint64_t k0, uint64_t k1,
+                     uint64_t offset, int64_t N, int64_t *out, void *stream);
+
+/* _ccf_kernel (samplers.py:100-107) for sorted U: W streamed once through
+ * shared memory by TMA bulk copies, each tile merged with its U range. */
+int dr_match_ccf(const double *W, int64_t M, const double *U, int64_t N, int64_t *out,
+                 void *stream);
+
+/* _dac_kernel (samplers.py:110-146) for sorted U; mode DRS_DAC_*. */
+int dr_match_dac(const double *W, const double *idx, int64_t M, const double *U, int64_t N,
+                 int64_t *out, int32_t mode, void *stream);
+
+/* _check_sorted_open (samplers.py:69-75): OUT_OF_SUPPORT / NOT_SORTED */
+int dr_check_sorted_open(const double *U, int64_t N, int32_t *status, void *stream);
+
+/* upper_bound_search / _upper_bound_nb (cdf.py:92-126, samplers.py:81-90):
+ * bisection on [lo,hi] with the reference's clamp-to-hi semantics;
+ * out[0] = index, out[1] = number of probes (OpStats.probes). */
+int dr_lower_bound_range(const double *W, int64_t lo, int64_t hi, double x, int64_t out[2],
+                         void *stream);
+
+/* Batched independent filters (config 4; the reference's per-filter loop
+ * over build_weight_table + dac_sampler): w[B][Mf] raw weights, keys[3B]
+ * (k0, k1, draw offset per filter) -> out[B][Nf]; U[B][Nf] and W[B][Mf]
+ * are written when non-NULL.  One CTA per filter, table held in shared
+ * memory.  status gets the OR over filters. */
+int dr_resample_batched(const double *w, int64_t B, int64_t Mf, int64_t Nf,
+                        const uint64_t *keys, double *W, double *U, int64_t *out,
+                        int32_t *status, void *stream);
+
+/* W-sharded table (config 5).
+ * Step 1 on every rank: local chained scan of the rank's shard.
+ *   S[Mg] local prefix sums, *Tg (device) = local total.  */
+int dr_shard_scan(const double *w_shard, int64_t Mg, double *S, double *Tg, int32_t *status,
+                  void *ws, size_t ws_bytes, void *stream);
+/* Step 2 after an all-gather of the G totals (device array totals[G]):
+ * W[j] = min((O_g + S[j]) / T, 1) in place, O_g and T folded in rank order;
+ * the last rank pins its last entry to 1.  Also builds idx of the shard. */
+int dr_shard_finalize(double *S_to_W, int64_t Mg, const double *totals, int32_t G, int32_t g,
+                      double *idx, void *stream);
+/* Step 3: the slice of the (replicated, identical on every rank) sorted U
+ * that lands in shard g: range[0] = #(U <= fl(O_g/T)) (0 for g = 0),
+ * range[1] = #(U <= fl(O_{g+1}/T)) (N for the last rank). */
+int dr_shard_range(const double *U, int64_t N, const double *totals, int32_t G, int32_t g,
+                   int64_t *range, void *stream);
+/* Step 4: out[i] = shard_start + lower bound of U[i] in the shard's W for
+ * range[0] <= i < range[1] (other entries untouched). */
+int dr_shard_match(const double *W, const double *idx, int64_t Mg, int64_t shard_start,
+                   const double *U, int64_t N, const int64_t *range, int64_t *out,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

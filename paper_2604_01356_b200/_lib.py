@@ -1,0 +1,151 @@
+"""ctypes boundary to libdrs.so (include/drs.h).
+
+The library is loaded from this package directory (built in-tree by
+``__graft_entry__.build()`` / ``make -C paper_2604_01356_b200/csrc``).  There is
+no fallback: a missing library or a missing CUDA device raises immediately.
+ctypes releases the GIL for the duration of every call; all calls are
+stream-ordered on torch's current stream of the current device.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import torch
+
+LIB_PATH = Path(__file__).resolve().with_name("libdrs.so")
+
+# status bits (include/drs.h)
+ST_INVALID_WEIGHT = 0x1
+ST_DEGENERATE = 0x2
+ST_ACCUM_OVERFLOW = 0x4
+ST_NOT_SORTED = 0x8
+ST_OUT_OF_SUPPORT = 0x10
+ST_REPAIRED = 0x20
+ST_NONFINITE = 0x40
+ST_DECREASING = 0x80
+ST_TOP_NOT_ONE = 0x100
+
+OP_TABLE = 1
+OP_SORTED = 2
+
+DAC_MODES = {"auto": 0, "merge": 1, "search": 2}
+
+_c_void_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_i32 = ctypes.c_int32
+_int = ctypes.c_int
+_size = ctypes.c_size_t
+_dbl = ctypes.c_double
+
+# name -> (restype, argtypes); mirrors include/drs.h
+_PROTOS = {
+    "dr_version": (ctypes.c_char_p, []),
+    "dr_strerror": (ctypes.c_char_p, [_int]),
+    "dr_scan_geometry": (None, [_c_void_p]),
+    "dr_workspace_bytes": (_size, [_int, _i64, _i64, _i64]),
+    "dr_workspace_init": (_int, [_c_void_p, _size, _c_void_p]),
+    "dr_index_entries": (_i64, [_i64]),
+    "dr_build_table": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_validate_table": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
+    "dr_build_index": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
+    "dr_uniforms": (_int, [_u64, _u64, _u64, _i64, _c_void_p, _c_void_p]),
+    "dr_sorted_uniforms": (_int, [_u64, _u64, _u64, _i64, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_sorted_uniforms_from": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_match_binary": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]),
+    "dr_sample_binary": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _i64, _c_void_p, _c_void_p]),
+    "dr_match_ccf": (_int, [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]),
+    "dr_match_dac": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i32, _c_void_p]),
+    "dr_check_sorted_open": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
+    "dr_lower_bound_range": (_int, [_c_void_p, _i64, _i64, _dbl, _c_void_p, _c_void_p]),
+    "dr_resample_batched": (_int, [_c_void_p, _i64, _i64, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "dr_shard_scan": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_shard_finalize": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
+    "dr_shard_range": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
+    "dr_shard_match": (_int, [_c_void_p, _c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p]),
+}
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load_library(path: Path | str | None = None):
+    """Load libdrs.so and bind the prototypes; raises if it is missing."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in _PROTOS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def lib():
+    """The bound library, after checking that a CUDA device is present."""
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2604_01356_b200 needs a CUDA device (sm_100a); none is visible")
+    return load_library()
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load_library().dr_strerror(rc).decode()
+        raise RuntimeError(f"{what} failed: {msg} ({rc})")
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def device() -> torch.device:
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def scan_geometry() -> tuple[int, ...]:
+    g = (ctypes.c_int32 * 5)()
+    load_library().dr_scan_geometry(ctypes.cast(g, ctypes.c_void_p))
+    return tuple(int(v) for v in g)
+
+
+class _Workspace:
+    __slots__ = ("tensor", "nbytes")
+
+    def __init__(self):
+        self.tensor = None
+        self.nbytes = 0
+
+
+_ws: dict[tuple[int, int], _Workspace] = {}
+_ws_lock = threading.Lock()
+
+
+def workspace(nbytes: int) -> tuple[int, int]:
+    """(pointer, size) of the look-back workspace of the current (device, stream).
+
+    Grown on demand; a new allocation is initialised with dr_workspace_init
+    on the stream it will be used on.
+    """
+    dev = torch.cuda.current_device()
+    st = stream_handle()
+    with _ws_lock:
+        w = _ws.setdefault((dev, st), _Workspace())
+        if w.nbytes < nbytes:
+            size = max(nbytes, 2 * w.nbytes, 1 << 16)
+            w.tensor = torch.empty(size, dtype=torch.uint8, device=device())
+            w.nbytes = size
+            check(lib().dr_workspace_init(w.tensor.data_ptr(), size, st), "dr_workspace_init")
+        return w.tensor.data_ptr(), w.nbytes

@@ -1,0 +1,55 @@
+"""Host/device marshalling for the drop-in API.
+
+Array-likes (lists, numpy arrays) are coerced exactly as the reference does
+(``np.ascontiguousarray(x, dtype=np.float64)``, samplers.py:168,199) and
+uploaded to the current CUDA device; CUDA tensors are used in place when they
+are contiguous float64 and 32-byte aligned (copied otherwise).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def is_device_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def to_device_f64(x) -> tuple[torch.Tensor, bool]:
+    """(1-D-or-not contiguous float64 CUDA tensor, input_was_host)."""
+    if is_device_tensor(x):
+        t = x
+        if t.dtype != torch.float64 or not t.is_contiguous() or t.data_ptr() % 32:
+            t = t.to(torch.float64).contiguous().clone()
+        return t, False
+    if isinstance(x, torch.Tensor):
+        x = x.detach().numpy()
+    a = np.ascontiguousarray(x, dtype=np.float64)
+    t = torch.empty(a.shape, dtype=torch.float64, device=_lib.device())
+    if a.size:
+        t.copy_(torch.from_numpy(a), non_blocking=False)
+    return t, True
+
+
+def empty_f64(n: int) -> torch.Tensor:
+    return torch.empty(int(n), dtype=torch.float64, device=_lib.device())
+
+
+def empty_i64(n: int) -> torch.Tensor:
+    return torch.empty(int(n), dtype=torch.int64, device=_lib.device())
+
+
+def status_word() -> torch.Tensor:
+    return torch.zeros(1, dtype=torch.int32, device=_lib.device())
+
+
+def read_status(st: torch.Tensor) -> int:
+    """Synchronising 4-byte read of a device status word."""
+    return int(st.item())
+
+
+def to_host(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().numpy()

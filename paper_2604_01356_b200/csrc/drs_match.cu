@@ -1,0 +1,312 @@
+// drs_match.cu -- the three inverse-CMF searches and their validators (sm_100a).
+//
+//   K4 match_binary / sample_binary  (samplers.py:93-97, 238-252)
+//        one lane per u, 16-ary descent of the table's index: one 128-byte
+//        line (4 x 256-bit loads) per level, W itself only at the last level.
+//   K5 match_ccf                     (samplers.py:100-107, 162-188)
+//        W streamed once: each CTA takes a 4096-entry W tile by TMA bulk copy
+//        into shared memory, finds its U range [#u <= W[j0-1], #u <= W[j1])
+//        by warp-cooperative 32-ary searches of U, and merges that range
+//        against the tile (bisection for the first u of a run, cursor for the rest).
+//   K6 match_dac                     (samplers.py:110-146, 191-210)
+//        divide step = the U-range split by W tiles (merge mode) or by index
+//        blocks (search mode); AUTO picks merge when M <= tau*N.
+// All three return the unique lower bound: first j with W[j] >= u (W[j] < u
+// compared strictly, ties to the first of an equal run), clamped to M-1.
+#include "drs_common.cuh"
+
+namespace drs {
+
+IndexDesc make_index_desc(int64_t M);  // drs_scan.cu
+
+constexpr int TW = 4096;   // W entries per merge tile (32 KB)
+constexpr int UCH = 4096;  // u results staged per chunk (32 KB)
+constexpr int64_t DAC_TAU = 16;
+
+static int launch_rc() {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
+// ------------------------------------------------------- K4 index search ----
+__global__ void __launch_bounds__(256) k_match_index(const double* __restrict__ W,
+                                                     const double* __restrict__ idx, IndexDesc d,
+                                                     const double* __restrict__ u, int64_t N,
+                                                     int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  out[i] = index_lower_bound(W, idx, d, __ldg(u + i));
+}
+
+// fused binary_sampler: the warp's 32 consecutive draws come from <= 9 Philox
+// blocks, computed once by lanes 0..8 and distributed by shuffles
+__global__ void __launch_bounds__(256) k_sample_binary(const double* __restrict__ W,
+                                                       const double* __restrict__ idx, IndexDesc d,
+                                                       uint64_t k0, uint64_t k1, uint64_t offset,
+                                                       int64_t N, int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+  if (base >= N) return;
+  const uint64_t d0 = offset + (uint64_t)base;
+  const uint64_t b0 = d0 >> 2;
+  U64x4 v{0, 0, 0, 0};
+  if (lane < 9) v = philox_block(k0, k1, b0 + (uint64_t)lane);
+  const uint64_t dd = d0 + (uint64_t)lane;
+  const int src = (int)((dd >> 2) - b0);
+  const uint64_t w0 = __shfl_sync(FULL, v.w0, src), w1 = __shfl_sync(FULL, v.w1, src);
+  const uint64_t w2 = __shfl_sync(FULL, v.w2, src), w3 = __shfl_sync(FULL, v.w3, src);
+  const int wi = (int)(dd & 3);
+  const uint64_t raw = wi == 0 ? w0 : (wi == 1 ? w1 : (wi == 2 ? w2 : w3));
+  const int64_t i = base + lane;
+  if (i < N) out[i] = index_lower_bound(W, idx, d, u01(raw));
+}
+
+// -------------------------------------------------------- K5 merge tiles ----
+// #(U[i] <= key) for sorted U, by a warp: 32-ary narrowing then one final probe.
+__device__ __forceinline__ int64_t warp_count_le(const double* __restrict__ U, int64_t N, double key) {
+  const int lane = threadIdx.x & 31;
+  int64_t lo = 0, hi = N;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int64_t step = cdiv(hi - lo, 32);
+    const int64_t p = lo + (int64_t)(lane + 1) * step - 1;
+    const bool pred = (p < hi) && (__ldg(U + p) <= key);
+    const int cnt = __popc(__ballot_sync(FULL, pred));
+    const int64_t nhi = lo + (int64_t)(cnt + 1) * step - 1;
+    lo = lo + (int64_t)cnt * step;
+    hi = nhi < hi ? nhi : hi;
+  }
+  const int64_t p = lo + lane;
+  const bool pred = (p < hi) && (__ldg(U + p) <= key);
+  return lo + __popc(__ballot_sync(FULL, pred));
+}
+
+// first p in [0,n) with a[p] >= x, clamped to n-1 (the reference's bisection)
+__device__ __forceinline__ int smem_lower_bound(const double* a, int n, double x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(256) k_merge_tiles(const double* __restrict__ W, int64_t M,
+                                                     const double* __restrict__ U, int64_t N,
+                                                     int64_t* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* sw = (double*)smraw;
+  int64_t* so = (int64_t*)(smraw + TW * sizeof(double));
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int64_t s_ib, s_ie;
+  const int64_t t = blockIdx.x;
+  const int64_t j0 = t * TW;
+  const int len = (int)((M - j0) < TW ? (M - j0) : TW);
+  const bool last = (j0 + len == M);
+  const int len_even = len & ~1;
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
+    if (len_even > 0) bulk_g2s(sw, W + j0, (uint32_t)len_even * 8u, &bar);
+  }
+  if (threadIdx.x == 64 && (len & 1)) sw[len - 1] = W[j0 + len - 1];
+  if (warp == 0) {
+    const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, __ldg(W + j0 - 1));
+    if ((threadIdx.x & 31) == 0) s_ib = v;
+  } else if (warp == 1) {
+    const int64_t v = last ? N : warp_count_le(U, N, __ldg(W + j0 + len - 1));
+    if ((threadIdx.x & 31) == 0) s_ie = v;
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int64_t ib = s_ib, ie = s_ie;
+  for (int64_t c0 = ib; c0 < ie; c0 += UCH) {
+    const int cl = (int)((ie - c0) < UCH ? (ie - c0) : UCH);
+    const int r = (cl + 255) / 256;
+    const int a = threadIdx.x * r;
+    const int b = (a + r < cl) ? (a + r) : cl;
+    if (a < b) {
+      double x = U[c0 + a];
+      int pos = smem_lower_bound(sw, len, x);
+      so[a] = j0 + pos;
+      for (int k = a + 1; k < b; ++k) {
+        x = U[c0 + k];
+        int steps = 0;
+        while (pos < len - 1 && sw[pos] < x && steps < 8) { ++pos; ++steps; }
+        if (pos < len - 1 && sw[pos] < x) pos = pos + 1 + smem_lower_bound(sw + pos + 1, len - pos - 1, x);
+        so[k] = j0 + pos;
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < cl; k += 256) out[c0 + k] = so[k];
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------------------------- checks ----
+__global__ void k_check_sorted_open(const double* __restrict__ U, int64_t N, int32_t* status) {
+  int bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += stride) {
+    if (i == 0 && (U[0] <= 0.0 || U[N - 1] > 1.0)) bad |= DRS_ST_OUT_OF_SUPPORT;
+    if (i > 0 && !(__dsub_rn(U[i], U[i - 1]) > 0.0)) bad |= DRS_ST_NOT_SORTED;
+  }
+  bad = __reduce_or_sync(FULL, bad);
+  if (bad && (threadIdx.x & 31) == 0) atomicOr(status, bad);
+}
+
+__global__ void k_validate_table(const double* __restrict__ W, int64_t M, int32_t* status) {
+  int bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += stride) {
+    const double v = W[i];
+    if (!(v > -dinf() && v < dinf())) bad |= DRS_ST_NONFINITE;
+    if (i == 0 && v < 0.0) bad |= DRS_ST_DECREASING;
+    if (i > 0 && __dsub_rn(v, W[i - 1]) < 0.0) bad |= DRS_ST_DECREASING;
+    if (i == M - 1 && v != 1.0) bad |= DRS_ST_TOP_NOT_ONE;
+  }
+  bad = __reduce_or_sync(FULL, bad);
+  if (bad && (threadIdx.x & 31) == 0) atomicOr(status, bad);
+}
+
+__global__ void k_build_index(const double* __restrict__ W, int64_t M, double* __restrict__ idx,
+                              IndexDesc d, int64_t total) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  int k = d.levels;
+  while (k > 1 && e < d.off[k]) --k;
+  const int64_t b = e - d.off[k];
+  int64_t span = 1;
+  for (int q = 0; q < k; ++q) span *= FANOUT;
+  double v = dinf();
+  if (b < d.n[k]) {
+    int64_t j = (b + 1) * span - 1;
+    if (j > M - 1) j = M - 1;
+    v = W[j];
+  }
+  idx[e] = v;
+}
+
+// upper_bound_search (cdf.py:92-126): bisection with the reference's probe count
+__global__ void k_lower_bound_range(const double* __restrict__ W, int64_t lo, int64_t hi, double x,
+                                    int64_t* out) {
+  int64_t a = lo, b = hi, probes = 0;
+  while (a != b) {
+    const int64_t m = (a + b) / 2;
+    ++probes;
+    if (W[m] < x) a = m + 1;
+    else b = m;
+  }
+  out[0] = a;
+  out[1] = probes;
+}
+
+static bool g_merge_attr = false;
+static int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
+                        cudaStream_t st) {
+  const int smem = TW * 8 + UCH * 8;
+  if (!g_merge_attr) {
+    cudaFuncSetAttribute(k_merge_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    g_merge_attr = true;
+  }
+  const int64_t tiles = cdiv(M, TW);
+  k_merge_tiles<<<(unsigned)tiles, 256, smem, st>>>(W, M, U, N, out);
+  return launch_rc();
+}
+
+int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st) {
+  const IndexDesc d = make_index_desc(M);
+  if (d.levels == 0) return DRS_OK;
+  if (!idx) return DRS_ERR_ARG;
+  const int64_t total = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
+  k_build_index<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(W, M, idx, d, total);
+  return launch_rc();
+}
+
+static int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
+                        int64_t* out, cudaStream_t st) {
+  const IndexDesc d = make_index_desc(M);
+  k_match_index<<<(unsigned)cdiv(N, 256), 256, 0, st>>>(W, idx, d, u, N, out);
+  return launch_rc();
+}
+
+}  // namespace drs
+
+using namespace drs;
+
+extern "C" {
+
+int dr_validate_table(const double* W, int64_t M, int32_t* status, void* stream) {
+  if (M < 1 || !W || !status) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
+  const int64_t blocks = cdiv(M, 256) < 148 * 8 ? cdiv(M, 256) : 148 * 8;
+  k_validate_table<<<(unsigned)blocks, 256, 0, st>>>(W, M, status);
+  return launch_rc();
+}
+
+int dr_build_index(const double* W, int64_t M, double* idx, void* stream) {
+  if (M < 1 || !W) return DRS_ERR_ARG;
+  return launch_build_index(W, M, idx, (cudaStream_t)stream);
+}
+
+int dr_match_binary(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
+                    int64_t* out, void* stream) {
+  if (M < 1 || N < 0 || !W || (N > 0 && (!u || !out))) return DRS_ERR_ARG;
+  if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
+  if (N == 0) return DRS_OK;
+  if (make_index_desc(M).levels > 0 && !idx) return DRS_ERR_ARG;
+  return launch_index(W, idx, M, u, N, out, (cudaStream_t)stream);
+}
+
+int dr_sample_binary(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
+                     uint64_t offset, int64_t N, int64_t* out, void* stream) {
+  if (M < 1 || N < 0 || !W || (N > 0 && !out)) return DRS_ERR_ARG;
+  if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
+  if (N == 0) return DRS_OK;
+  const IndexDesc d = make_index_desc(M);
+  if (d.levels > 0 && !idx) return DRS_ERR_ARG;
+  k_sample_binary<<<(unsigned)cdiv(N, 256), 256, 0, (cudaStream_t)stream>>>(W, idx, d, k0, k1,
+                                                                           offset, N, out);
+  return launch_rc();
+}
+
+int dr_match_ccf(const double* W, int64_t M, const double* U, int64_t N, int64_t* out, void* stream) {
+  if (M < 1 || N < 0 || !W || (N > 0 && (!U || !out))) return DRS_ERR_ARG;
+  if ((uintptr_t)W & 15) return DRS_ERR_ALIGN;
+  if (N == 0) return DRS_OK;
+  return launch_merge(W, M, U, N, out, (cudaStream_t)stream);
+}
+
+int dr_match_dac(const double* W, const double* idx, int64_t M, const double* U, int64_t N,
+                 int64_t* out, int32_t mode, void* stream) {
+  if (M < 1 || N < 0 || !W || (N > 0 && (!U || !out))) return DRS_ERR_ARG;
+  if (mode != DRS_DAC_AUTO && mode != DRS_DAC_MERGE && mode != DRS_DAC_SEARCH) return DRS_ERR_MODE;
+  if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
+  if (N == 0) return DRS_OK;
+  bool merge = (mode == DRS_DAC_MERGE) || (mode == DRS_DAC_AUTO && M <= DAC_TAU * N);
+  if (!merge && make_index_desc(M).levels > 0 && !idx) merge = true;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (merge) return launch_merge(W, M, U, N, out, st);
+  return launch_index(W, idx, M, U, N, out, st);
+}
+
+int dr_check_sorted_open(const double* U, int64_t N, int32_t* status, void* stream) {
+  if (N < 0 || !status || (N > 0 && !U)) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
+  if (N == 0) return DRS_OK;
+  const int64_t blocks = cdiv(N, 256) < 148 * 8 ? cdiv(N, 256) : 148 * 8;
+  k_check_sorted_open<<<(unsigned)blocks, 256, 0, st>>>(U, N, status);
+  return launch_rc();
+}
+
+int dr_lower_bound_range(const double* W, int64_t lo, int64_t hi, double x, int64_t* out,
+                         void* stream) {
+  if (!W || !out || lo < 0 || hi < lo) return DRS_ERR_ARG;
+  k_lower_bound_range<<<1, 1, 0, (cudaStream_t)stream>>>(W, lo, hi, x, out);
+  return launch_rc();
+}
+
+}  // extern "C"

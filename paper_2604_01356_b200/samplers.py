@@ -1,0 +1,205 @@
+"""The three multinomial samplers on the GPU (drop-in for dacresample.samplers).
+
+Mirrors /root/reference/pkg/src/dacresample/samplers.py: matchers
+``ccf_match`` (:162-188) and ``dac_match`` (:191-210), samplers
+``binary_sampler`` (:238-252), ``ccf_sampler`` (:255-259), ``dac_sampler``
+(:262-266), ``linear_oracle`` (:49-66), ``OpStats`` (:40-46) and
+``warm_kernels`` (:149-156).  Same names, arguments, return dtype (int64,
+0-based) and error messages.
+
+Host inputs (lists, numpy) give numpy results, CUDA-tensor inputs give CUDA
+tensors; samplers return numpy unless ``device=True``.  Every index is the
+unique lower bound ``min{j : W[j] >= u}`` computed on the device -- the
+samplers differ in search strategy only, exactly as in the reference.
+``stats=`` (operation counting, a CPU-instrumentation feature) is supported
+by ``upper_bound_search`` and ``linear_oracle``; the matchers and samplers
+raise NotImplementedError for it rather than falling back to the CPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import empty_i64, is_device_tensor, read_status, status_word, to_device_f64
+from .cdf import WeightTable
+from .randkit import RngStream, sorted_uniforms_device
+
+__all__ = [
+    "OpStats",
+    "linear_oracle",
+    "binary_sampler",
+    "ccf_match",
+    "ccf_sampler",
+    "dac_match",
+    "dac_sampler",
+    "warm_kernels",
+]
+
+
+@dataclass
+class OpStats:
+    """Operation tallies for verifying complexity claims without a clock."""
+
+    comparisons: int = 0  # weight-vs-uniform comparisons in linear scans
+    probes: int = 0       # bisection midpoint evaluations
+    max_depth: int = 0    # deepest divide-and-conquer scope nesting
+
+
+def _no_stats(stats, name):
+    if stats is not None:
+        raise NotImplementedError(
+            f"{name}(stats=...) counts CPU operations of the reference's instrumented "
+            "twin; the GPU path does not count and never falls back to the CPU"
+        )
+
+
+def _lower_bounds(table: WeightTable, u: torch.Tensor) -> torch.Tensor:
+    out = empty_i64(u.numel())
+    if u.numel():
+        _lib.check(
+            _lib.lib().dr_match_binary(
+                table.device_cum.data_ptr(), _ptr(table.device_index), table.size,
+                u.data_ptr(), u.numel(), out.data_ptr(), _lib.stream_handle(),
+            ),
+            "dr_match_binary",
+        )
+    return out
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def linear_oracle(table: WeightTable, u: float, stats=None) -> int:
+    """Reference inverse CDF: first j with cum[j] >= u (samplers.py:49-66).
+
+    The answer is the same lower bound as every sampler; the comparison
+    count of the reference's linear scan is j + 1.
+    """
+    u = float(u)
+    if not 0.0 < u <= 1.0:
+        raise ValueError("u must lie in (0, 1]")
+    x = torch.full((1,), u, dtype=torch.float64, device=_lib.device())
+    j = int(_lower_bounds(table, x).item())
+    if stats is not None:
+        stats.comparisons += j + 1
+    return j
+
+
+def _check_sorted_open(u: torch.Tensor) -> None:
+    """samplers.py:69-75 on the device; raises with the reference's messages."""
+    if u.numel() == 0:
+        return
+    st = status_word()
+    _lib.check(_lib.lib().dr_check_sorted_open(u.data_ptr(), u.numel(), st.data_ptr(), _lib.stream_handle()),
+               "dr_check_sorted_open")
+    s = read_status(st)
+    if s & _lib.ST_OUT_OF_SUPPORT:
+        raise ValueError("uniforms must lie in (0, 1]")
+    if s & _lib.ST_NOT_SORTED:
+        raise ValueError("input not sorted")
+
+
+def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto"):
+    host = not is_device_tensor(u)
+    ud, _ = to_device_f64(u)
+    if ud.ndim != 1:
+        ud = ud.reshape(-1)
+    if check:
+        _check_sorted_open(ud)
+    n = ud.numel()
+    out = empty_i64(n)
+    if n:
+        L = _lib.lib()
+        s = _lib.stream_handle()
+        W = table.device_cum
+        if kind == "ccf":
+            rc = L.dr_match_ccf(W.data_ptr(), table.size, ud.data_ptr(), n, out.data_ptr(), s)
+        else:
+            rc = L.dr_match_dac(W.data_ptr(), _ptr(table.device_index), table.size, ud.data_ptr(), n,
+                                out.data_ptr(), _lib.DAC_MODES[mode], s)
+        _lib.check(rc, f"dr_match_{kind}")
+    return out.cpu().numpy() if host else out
+
+
+def ccf_match(u, table: WeightTable, stats: OpStats | None = None, check: bool = True):
+    """Match sorted uniforms against the table by a streaming merge (samplers.py:162-188).
+
+    The table is read once, tile by tile (TMA bulk copies into shared
+    memory); each tile merges with the slice of u that lands in it.
+    """
+    _no_stats(stats, "ccf_match")
+    return _match("ccf", u, table, check)
+
+
+def dac_match(u, table: WeightTable, stats: OpStats | None = None, check: bool = True,
+              *, mode: str = "auto"):
+    """Match sorted uniforms by divide and conquer (samplers.py:191-210).
+
+    ``mode``: "merge" splits u by table tiles and merges each slice (reads
+    all of W); "search" splits by index blocks and bisects per u (reads
+    O(N log(M/N)) lines); "auto" picks merge when M <= 16 N.
+    """
+    _no_stats(stats, "dac_match")
+    if mode not in _lib.DAC_MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    return _match("dac", u, table, check, mode)
+
+
+def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
+                   *, device: bool = False):
+    """n independent draws, each by a full-range search; draw order kept (samplers.py:238-252)."""
+    _no_stats(stats, "binary_sampler")
+    n = int(n)
+    if n < 0:
+        raise ValueError("negative dimensions are not allowed")
+    out = empty_i64(n)
+    if n:
+        L = _lib.lib()
+        s = _lib.stream_handle()
+        W = table.device_cum
+        if isinstance(stream, RngStream):
+            off = stream._take(n)
+            rc = L.dr_sample_binary(W.data_ptr(), _ptr(table.device_index), table.size,
+                                    stream.key[0], stream.key[1], off, n, out.data_ptr(), s)
+            _lib.check(rc, "dr_sample_binary")
+        else:
+            us, _ = to_device_f64(stream.uniforms(n))
+            out = _lower_bounds(table, us)
+    return out if device else out.cpu().numpy()
+
+
+def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto"):
+    _no_stats(stats, f"{kind}_sampler")
+    n = int(n)
+    U = sorted_uniforms_device(stream, n)
+    out = _match(kind, U, table, check=False, mode=mode)
+    return out if device else out.cpu().numpy()
+
+
+def ccf_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
+                *, device: bool = False):
+    """Sorted uniforms + streaming merge: multinomial(w, n) in O(M + N) (samplers.py:255-259)."""
+    return _sorted_sampler("ccf", table, n, stream, stats, device)
+
+
+def dac_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
+                *, device: bool = False, mode: str = "auto"):
+    """Sorted uniforms + divide-and-conquer (samplers.py:262-266)."""
+    if mode not in _lib.DAC_MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    return _sorted_sampler("dac", table, n, stream, stats, device, mode)
+
+
+def warm_kernels() -> None:
+    """Load the library and run every search kernel once (samplers.py:149-156)."""
+    t = WeightTable([0.5, 1.0])
+    u = torch.tensor([0.25, 0.75], dtype=torch.float64, device=_lib.device())
+    ccf_match(u, t, check=False)
+    dac_match(u, t, check=False)
+    _lower_bounds(t, u)
+    torch.cuda.current_stream().synchronize()

@@ -1,0 +1,314 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle and the reference.
+
+Exact mode: given the reference's own W and U, every sampler's indices must
+equal the reference's bit for bit.  Device mode: W and U computed on the GPU
+must equal the oracle's device-association twins bit for bit, and differ
+from the reference only by fp64 reassociation (ulp drift reported; index
+flips only where u sits within the drift of a boundary).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import (
+    PhiloxStream,
+    ReplayStream,
+    boundary_query_set,
+    enumerate_weight_tables,
+    golden_cases,
+    linear_scan_bulk,
+    reference_table_exact,
+    ulps,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+
+
+# ---------------------------------------------------------------- exact mode
+def test_exact_mode_reference_cases(drs, golden):
+    n = 0
+    for W, u, e in golden_cases(golden):
+        t = drs.WeightTable(W)
+        np.testing.assert_array_equal(drs.ccf_match(u, t), e)
+        np.testing.assert_array_equal(drs.dac_match(u, t), e)
+        np.testing.assert_array_equal(drs.dac_match(u, t, mode="merge"), e)
+        np.testing.assert_array_equal(drs.dac_match(u, t, mode="search"), e)
+        np.testing.assert_array_equal(drs.binary_sampler(t, u.shape[0], ReplayStream(u)), e)
+        n += 1
+    assert n == 300
+
+
+def test_exact_mode_exhaustive_tables(drs):
+    for raw in enumerate_weight_tables(6):
+        W = reference_table_exact(raw)
+        t = drs.WeightTable(W)
+        u = boundary_query_set(W)
+        e = linear_scan_bulk(W, u)
+        np.testing.assert_array_equal(drs.ccf_match(u, t), e)
+        np.testing.assert_array_equal(drs.dac_match(u, t, mode="merge"), e)
+        np.testing.assert_array_equal(drs.dac_match(u, t, mode="search"), e)
+        np.testing.assert_array_equal(drs.binary_sampler(t, u.shape[0], ReplayStream(u)), e)
+
+
+def test_exact_mode_c1(drs, golden, orc):
+    W = golden[f"tbl_cum_{int(golden['tbl_count']) - 1}"]
+    t = drs.WeightTable(W)
+    d = PhiloxStream(2001).uniforms(1025)
+    U, _ = orc.sorted_from_z(-np.log(d), 1024, association="port")  # the reference's U
+    np.testing.assert_array_equal(drs.dac_match(U, t), golden["c1_dac"])
+    np.testing.assert_array_equal(drs.ccf_match(U, t), golden["c1_ccf"])
+    np.testing.assert_array_equal(drs.binary_sampler(t, 1024, ReplayStream(d[:1024])), golden["c1_binary"])
+
+
+def test_exact_mode_large_random(drs, orc):
+    rng = np.random.default_rng(77)
+    for M, N in [(1 << 20, 1 << 20), (1 << 22, 1 << 14), (300001, 4097), (5, 100000)]:
+        w = np.exp(3 * rng.standard_normal(M))
+        w[rng.random(M) < 0.2] = 0.0
+        W, _ = orc.port_build_table(w)
+        U = np.sort(rng.random(N))
+        U = U[U > 0]
+        k = min(N // 4, M)
+        U[: k] = np.sort(rng.choice(W[W > 0], size=k))  # exact boundaries
+        U = np.sort(U)
+        e = orc.match("binary", W, U)
+        t = drs.WeightTable(W)
+        Ud = dev(U)
+        for mode in ("merge", "search", "auto"):
+            np.testing.assert_array_equal(drs.dac_match(Ud, t, check=False, mode=mode).cpu().numpy(), e)
+        np.testing.assert_array_equal(drs.ccf_match(Ud, t, check=False).cpu().numpy(), e)
+        perm = rng.permutation(U.shape[0])
+        np.testing.assert_array_equal(drs.binary_sampler(t, U.shape[0], ReplayStream(U[perm])), e[perm])
+
+
+def test_clamp_and_ties(drs):
+    t = drs.WeightTable([0.25, 0.25, 0.5, 1.0, 1.0, 1.0])
+    u = np.array([1e-300, 0.25, 0.2500000001, 0.5, 1.0])
+    e = np.array([0, 0, 2, 2, 3])
+    np.testing.assert_array_equal(drs.ccf_match(u, t), e)
+    np.testing.assert_array_equal(drs.dac_match(u, t, mode="search"), e)
+    # u > 1 (check=False): the reference's bisection clamps to M-1
+    ud = dev([0.9, 1.5])
+    assert drs.dac_match(ud, t, check=False, mode="search").tolist() == [3, 5]
+    assert drs.dac_match(ud, t, check=False, mode="merge").tolist() == [3, 5]
+
+
+# --------------------------------------------------------------- device mode
+def test_build_table_bit_exact_vs_oracle(drs, orc, golden):
+    for i in range(int(golden["tbl_count"])):
+        raw = golden[f"tbl_raw_{i}"]
+        t = drs.build_weight_table(raw)
+        W, _ = orc.build_table(raw)
+        np.testing.assert_array_equal(t.cum, W)
+        np.testing.assert_array_equal(t.device_index.cpu().numpy() if t.device_index is not None else np.empty(0),
+                                      orc.build_index(W))
+        ref = golden[f"tbl_cum_{i}"]
+        assert np.abs(t.cum - ref).max() <= 1e-12
+
+
+@pytest.mark.parametrize("M", [1, 2, 31, 33, 8447, 8448, 8449, 3 * 8448 + 5, 1 << 20, (1 << 22) + 3])
+def test_build_table_tile_edges(drs, orc, M):
+    rng = np.random.default_rng(M)
+    w = rng.random(M)
+    w[rng.random(M) < 0.1] = 0.0
+    if w.sum() == 0:
+        w[0] = 1
+    t = drs.build_weight_table(w)
+    W, _ = orc.build_table(w)
+    np.testing.assert_array_equal(t.cum, W)
+    assert t.cum[-1] == 1.0 and np.all(np.diff(t.cum) >= 0)
+
+
+def test_build_table_errors(drs):
+    with pytest.raises(ValueError, match="empty distribution"):
+        drs.build_weight_table([])
+    with pytest.raises(ValueError, match="empty distribution"):
+        drs.build_weight_table(np.ones((2, 2)))
+    with pytest.raises(ValueError, match="degenerate distribution"):
+        drs.build_weight_table([0.0, 0.0])
+    for bad in ([-1.0, 2.0], [np.nan], [np.inf, 1.0]):
+        with pytest.raises(ValueError, match="invalid weight"):
+            drs.build_weight_table(bad)
+    with pytest.raises(ValueError, match="accumulation overflow"):
+        drs.build_weight_table([1e308, 1e308])
+
+
+def test_sorted_uniforms_bit_exact_vs_oracle(drs, orc, golden):
+    for i, (seed, n) in enumerate(golden["su_cases"]):
+        s = drs.RngStream(int(seed))
+        U = drs.sorted_uniforms(s, int(n))
+        assert s.draws == int(n) + 1
+        k0, k1 = orc.key_of(int(seed))
+        Uo, _ = orc.sorted_uniforms(k0, k1, 0, int(n))
+        np.testing.assert_array_equal(U, Uo)
+        # against the reference (PCG64 replaced by the same Philox draws): reassociation + log ulp only
+        ref = golden[f"su_U_{i}"]
+        assert np.abs(U - ref).max() <= 1e-13
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 1022, 1023, 1024, 1025, 4095, 70001, 1 << 20])
+def test_sorted_uniforms_sizes(drs, orc, n):
+    s = drs.RngStream(n, (3,))
+    s.uniforms(5)  # non-multiple-of-4 draw offset
+    U = drs.sorted_uniforms(s, n)
+    k0, k1 = orc.key_of(n, (3,))
+    Uo, _ = orc.sorted_uniforms(k0, k1, 5, n)
+    np.testing.assert_array_equal(U, Uo)
+    assert U[0] > 0 and U[-1] < 1 and np.all(np.diff(U) > 0)
+
+
+def test_replay_and_repair_bit_exact(drs, orc, golden):
+    for i in range(int(golden["rp_count"])):
+        d = golden[f"rp_draws_{i}"]
+        n = d.shape[0] - 1
+        U = drs.sorted_uniforms(ReplayStream(d), n)
+        Uo, _ = orc.sorted_uniforms_from(d, n)
+        np.testing.assert_array_equal(U, Uo)
+        assert U[0] > 0 and U[-1] < 1 and np.all(np.diff(U) > 0)
+        assert np.abs(U - golden[f"rp_U_{i}"]).max() <= 1e-12
+    u = drs.sorted_uniforms(ReplayStream([0.5, 0.5, 0.5]), 2)
+    np.testing.assert_allclose(u, [1 / 3, 2 / 3], rtol=1e-15)
+
+
+def test_repair_many_sites(drs, orc):
+    rng = np.random.default_rng(5)
+    d = rng.random(50001)
+    d[rng.random(50001) < 0.3] = 1 - 2.0 ** -53  # thousands of vanishing spacings
+    U = drs.sorted_uniforms(ReplayStream(d), 50000)
+    Uo, st = orc.sorted_uniforms_from(d, 50000)
+    assert st & 0x20
+    np.testing.assert_array_equal(U, Uo)
+
+
+def test_uniforms_match_numpy_philox(drs):
+    s = drs.RngStream(2003)
+    a = s.uniforms(7)
+    b = s.uniforms(1000)
+    gen = np.random.Generator(np.random.Philox(np.random.SeedSequence(2003)))
+    np.testing.assert_array_equal(np.concatenate([a, b]), gen.random(1007))
+    assert s.draws == 1007
+
+
+def test_binary_sampler_bit_exact_vs_oracle(drs, orc):
+    w = np.exp(2 * np.random.default_rng(8).standard_normal(100000))
+    t = drs.build_weight_table(w)
+    s = drs.RngStream(31)
+    s.uniforms(3)
+    out = drs.binary_sampler(t, 50001, s)
+    k0, k1 = orc.key_of(31)
+    u = orc.uniforms(k0, k1, 3, 50001)
+    np.testing.assert_array_equal(out, orc.match("binary", t.cum, u))
+
+
+@pytest.mark.parametrize("M,N", [(65536, 1024), (1 << 20, 1 << 20), (1 << 24, 1 << 12), (1000, 1 << 18)])
+def test_samplers_device_mode_vs_oracle(drs, orc, M, N):
+    w = np.exp(np.random.default_rng(M + N).standard_normal(M))
+    t = drs.build_weight_table(w)
+    W, _ = orc.build_table(w)
+    np.testing.assert_array_equal(t.cum, W)
+    k0, k1 = orc.key_of(N)
+    Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+    e = orc.match("dac", W, Uo)
+    for fn in (drs.dac_sampler, drs.ccf_sampler):
+        np.testing.assert_array_equal(fn(t, N, drs.RngStream(N)), e)
+    for mode in ("merge", "search"):
+        np.testing.assert_array_equal(drs.dac_sampler(t, N, drs.RngStream(N), mode=mode), e)
+
+
+def test_device_vs_reference_flips_only_near_boundaries(drs, orc):
+    """Device-mode disagreement with the reference association is confined to
+    u within the measured reassociation drift of a boundary W_j."""
+    M, N = 1 << 20, 1 << 16
+    w = np.exp(4 * np.random.default_rng(1003).standard_normal(M))
+    t = drs.build_weight_table(w)
+    Wref, _ = orc.port_build_table(w)
+    s = drs.RngStream(2003)
+    U = drs.sorted_uniforms(drs.RngStream(2003), N)
+    d = PhiloxStream(2003).uniforms(N + 1)
+    Uref, _ = orc.sorted_from_z(-np.log(d), N, association="port")
+    out = drs.dac_sampler(t, N, s)
+    eref = orc.match("dac", Wref, Uref)
+    drift_W = np.abs(t.cum - Wref).max()
+    drift_U = np.abs(U - Uref).max()
+    flips = np.nonzero(out != eref)[0]
+    near = np.abs(Wref[eref[flips]] - Uref[flips]) <= 2 * (drift_W + drift_U) + 1e-300
+    near |= np.abs(Wref[np.maximum(eref[flips] - 1, 0)] - Uref[flips]) <= 2 * (drift_W + drift_U)
+    assert near.all(), (flips, drift_W, drift_U)
+
+
+def test_chi_square_counts(drs):
+    rng = np.random.default_rng(40)
+    for raw in (rng.random(16), np.full(16, 1 / 16)):
+        t = drs.build_weight_table(raw)
+        expected = 1_000_000 * t.weights()
+        for fn in (drs.binary_sampler, drs.ccf_sampler, drs.dac_sampler):
+            counts = np.bincount(fn(t, 1_000_000, drs.RngStream(41)), minlength=16)
+            chi2 = float(((counts - expected) ** 2 / expected).sum())
+            assert chi2 < 37.70
+
+
+def test_zero_weight_never_drawn(drs):
+    t = drs.build_weight_table([0.0, 0.3, 0.0, 0.7, 0.0])
+    for fn in (drs.binary_sampler, drs.ccf_sampler, drs.dac_sampler):
+        c = np.bincount(fn(t, 1_000_000, drs.RngStream(17)), minlength=5)
+        assert c[[0, 2, 4]].sum() == 0
+
+
+# ---------------------------------------------------------- batched / sharded
+def test_batched_bit_exact_vs_oracle(drs, orc):
+    rng = np.random.default_rng(1004)
+    B, Mf, Nf = 64, 16384, 256
+    pi = rng.dirichlet(np.ones(64), size=B)
+    q = rng.chisquare(6, size=(B, 256, 64))
+    w = np.exp(np.log(1 / 256) + np.log(pi)[:, None, :] - 0.5 * q).reshape(B, Mf)
+    streams = [drs.RngStream(2004, (b,)) for b in range(B)]
+    for s in streams[::3]:
+        s.uniforms(1)
+    keys = np.array([[s.key[0], s.key[1], s.position] for s in streams], dtype=np.uint64)
+    out, U, W = drs.resample_batched(w, Nf, streams, return_uniforms=True, return_tables=True)
+    eo, Uo, Wo, st = orc.resample_batched(w, Nf, keys)
+    np.testing.assert_array_equal(W, Wo)
+    np.testing.assert_array_equal(U, Uo)
+    np.testing.assert_array_equal(out, eo)
+    # identical to the single-filter path
+    t = drs.build_weight_table(w[5])
+    np.testing.assert_array_equal(t.cum, W[5])
+
+
+def test_sharded_single_gpu_emulation(drs, orc):
+    """The shard steps for G shards run one after another on one GPU, with the
+    all-gather replaced by stacking the totals; result == oracle sharded table."""
+    from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable
+
+    ops = DeviceShardOps()
+    rng = np.random.default_rng(1005)
+    M, N = 1 << 20, 1 << 14
+    w = np.exp(2 * rng.standard_normal(M))
+    off = rng.integers(0, M - 1024)
+    w[off:off + 1024] = (w.sum() - w[off:off + 1024].sum()) / 3 / 1024
+    for G in (1, 2, 4):
+        parts = [dev(w[M * g // G: M * (g + 1) // G]) for g in range(G)]
+        scans = [ops.shard_scan(p) for p in parts]
+        totals = torch.cat([s[1] for s in scans])
+        Wo, To, st = orc.build_table_sharded(w, G)
+        np.testing.assert_array_equal(totals.cpu().numpy(), To)
+        full = torch.full((N,), -1, dtype=torch.int64, device="cuda")
+        Ws = []
+        for g in range(G):
+            W, idx = ops.finalize(scans[g][0], totals, G, g)
+            Ws.append(W.cpu().numpy())
+            tab = ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g, world=G)
+            U = ops.sorted_uniforms(drs.RngStream(2005), N)
+            rngd = ops.shard_range(U, totals, G, g)
+            o = ops.shard_match(tab, U, rngd)
+            a, b = rngd.tolist()
+            full[a:b] = o[a:b]
+        np.testing.assert_array_equal(np.concatenate(Ws), Wo)
+        k0, k1 = orc.key_of(2005)
+        Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+        np.testing.assert_array_equal(full.cpu().numpy(), orc.match("dac", Wo, Uo))
