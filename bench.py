@@ -195,11 +195,35 @@ def run_drs(args, rank, world, local_rank):
         samples = N
         sampler = {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}[args.sampler]
         kw = {"mode": args.mode} if args.sampler == "dac" else {}
+        out_buf = torch.empty(N, dtype=torch.int64, device=dev)
+        if args.sampler != "binary":
+            kw["uniforms_out"] = torch.empty(N, dtype=torch.float64, device=dev)
 
-        def step():
-            return sampler(table, N, stream, device=True, **kw)
+        def eager_step():
+            return sampler(table, N, stream, device=True, out=out_buf, **kw)
 
-        launches_per_step = 1 if args.sampler == "binary" else 3
+        step = eager_step
+        fused = args.sampler == "dac" and args.mode != "merge" and M > 16 * N and (N + 1) <= 148 * 1024
+        launches_per_step = {"binary": 1, "ccf": 3}.get(args.sampler, 1 if fused else 3)
+        if args.graph:
+            # one sampler call captured once; the stream position lives on the
+            # device, so every replay draws fresh uniforms
+            dstream = drs.DeviceRngStream(c["useed"], (rank,))
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                sampler(table, N, dstream, device=True, out=out_buf, **kw)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=side):
+                    sampler(table, N, dstream, device=True, out=out_buf, **kw)
+            torch.cuda.current_stream().wait_stream(side)
+            if args.sampler == "binary":
+                launches_per_step += 1  # the device-side stream advance
+            elif not fused:
+                launches_per_step += 1
+
+            def step():
+                graph.replay()
         # the dominant kernel alone: the search over a fixed U
         U = drs.randkit.sorted_uniforms_device(drs.RngStream(c["useed"], (rank, 7)), N)
         match = {"dac": lambda: drs.dac_match(U, table, check=False, mode=args.mode),
@@ -214,22 +238,28 @@ def run_drs(args, rank, world, local_rank):
         step()
         kernel_step()
     torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+
+    def timed(fn, k):
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        for i in range(k):
+            l2_flush()
+            starts[i].record(s)
+            fn()
+            ends[i].record(s)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in zip(starts, ends)]
 
     # ---- timed region: per-step events, L2 flushed before each step
-    s = torch.cuda.current_stream()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
-        for i in range(args.steps):
-            l2_flush()
-            starts[i].record(s)
-            step()
-            ends[i].record(s)
-        torch.cuda.synchronize()
+        step_ms = timed(step, args.steps)
     barrier()
-    step_ms = [a.elapsed_time(b) for a, b in zip(starts, ends)]
+    eager_ms = None
+    if step is not locals().get("eager_step", step):
+        eager_ms = statistics.median(timed(eager_step, args.steps))
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -298,6 +328,9 @@ def run_drs(args, rank, world, local_rank):
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
+        "timing": "CUDA-graph replay of one sampler call (device-resident stream position)"
+                  if eager_ms is not None else "eager public-API calls",
+        "eager_ms_per_step_median": eager_ms,
     }
     return line, (alg_bytes, samples)
 
@@ -355,6 +388,8 @@ def main():
     ap.add_argument("--impl", default="drs", choices=["drs", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time eager API calls instead of CUDA-graph replays")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 

@@ -113,6 +113,34 @@ int dr_match_binary(const double *W, const double *idx, int64_t M, const double 
 int dr_sample_binary(const double *W, const double *idx, int64_t M, uint64_t k0, uint64_t k1,
                      uint64_t offset, int64_t N, int64_t *out, void *stream);
 
+/* dac_sampler (samplers.py:262-266) in one call: sorted uniforms from the
+ * stream (k0,k1) at `offset` -- or at *offset_dev when offset_dev is non-NULL,
+ * which is then advanced by N+1 on the device (CUDA-graph replayable) --
+ * then the divide-and-conquer search.  For N+1 <= 1024 x (co-resident CTAs)
+ * and mode SEARCH/AUTO-sparse this is ONE cooperative kernel; otherwise the
+ * two-pass sorted uniforms followed by dr_match_dac.  U[N] receives the
+ * sorted uniforms, out[N] the indices, status REPAIRED when the repair ran. */
+int dr_sample_dac(const double *W, const double *idx, int64_t M, uint64_t k0, uint64_t k1,
+                  uint64_t offset, uint64_t *offset_dev, int64_t N, double *U, int64_t *out,
+                  int32_t *status, int32_t mode, void *ws, size_t ws_bytes, void *stream);
+
+/* dr_sample_dac with the N+1 underlying uniforms supplied (raw[N+1], a
+ * duck-typed host stream such as the reference tests' ReplayStream). */
+int dr_sample_dac_from(const double *W, const double *idx, int64_t M, const double *raw, int64_t N,
+                       double *U, int64_t *out, int32_t *status, int32_t mode, void *ws,
+                       size_t ws_bytes, void *stream);
+
+/* ccf_sampler (samplers.py:255-259): sorted uniforms then the streaming merge. */
+int dr_sample_ccf(const double *W, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,
+                  uint64_t *offset_dev, int64_t N, double *U, int64_t *out, int32_t *status,
+                  void *ws, size_t ws_bytes, void *stream);
+
+/* binary_sampler with a device-resident stream position (*offset_dev, advanced
+ * by N) and the top index levels staged in shared memory. */
+int dr_sample_binary_dev(const double *W, const double *idx, int64_t M, uint64_t k0, uint64_t k1,
+                         uint64_t offset, uint64_t *offset_dev, int64_t N, int64_t *out,
+                         void *stream);
+
 /* _ccf_kernel (samplers.py:100-107) for sorted U: W streamed once through
  * shared memory by TMA bulk copies, each tile merged with its U range. */
 int dr_match_ccf(const double *W, int64_t M, const double *U, int64_t N, int64_t *out,

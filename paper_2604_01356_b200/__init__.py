@@ -14,7 +14,7 @@ over several GPUs with a single all-gather of shard totals).
 
 from .batched import resample_batched
 from .cdf import WeightTable, build_weight_table, upper_bound_search
-from .randkit import RngStream, sorted_uniforms, uniform_open
+from .randkit import DeviceRngStream, RngStream, sorted_uniforms, uniform_open
 from .samplers import (
     OpStats,
     binary_sampler,
@@ -29,6 +29,7 @@ from .sharded import ShardedWeightTable, build_sharded_table, sharded_dac_sample
 
 __all__ = [
     "RngStream",
+    "DeviceRngStream",
     "uniform_open",
     "sorted_uniforms",
     "WeightTable",

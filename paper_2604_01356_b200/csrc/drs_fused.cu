@@ -1,0 +1,533 @@
+// drs_fused.cu -- dac_sampler / binary_sampler as ONE kernel launch (sm_100a).
+//
+// dac_sampler (samplers.py:262-266) = sorted_uniforms (randkit.py:70-101)
+// followed by dac_match (samplers.py:191-210).  For N+1 <= (co-resident
+// CTAs) * 1024 the whole call is one cooperative launch:
+//
+//   1. thread 0 TMA-prefetches the top levels of the table's search index
+//      (a contiguous suffix of idx, <= 64 KB) into shared memory;
+//   2. every thread draws its 4 Philox uniforms, z = -log u, and the CTA
+//      forms its tile of the chained scan (identical association to
+//      dr_sorted_uniforms, so U is bit-identical to the two-pass path);
+//   3. one grid barrier; each CTA folds the tile totals before it (the same
+//      left fold the look-back computes) and the spacing minimum;
+//   4. U = Z / Z[n] in registers; the rare collapse repair runs behind two
+//      more grid barriers only when the reference's exactness check fires;
+//   5. each thread searches its 4 sorted u's: the top index levels from
+//      shared memory, the lower ones as one 128-byte line (4 x 256-bit
+//      loads) per level, W last -- O(N log_16 M) lines instead of 8M bytes;
+//   6. indices (and optionally U) are written coalesced.
+// The stream position may live in device memory (offset_dev) and is then
+// advanced on the device, so the launch can be captured in a CUDA graph
+// and replayed with fresh draws each time.
+#include <cooperative_groups.h>
+
+#include "drs_common.cuh"
+
+namespace drs {
+
+IndexDesc make_index_desc(int64_t M);
+int64_t ws_capacity_tiles(size_t ws_bytes);
+ScanWS carve_ws(void* ws, size_t ws_bytes);
+int sorted_uniforms_launch(uint64_t k0, uint64_t k1, uint64_t offset, const uint64_t* offset_dev,
+                           int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes,
+                           cudaStream_t st);
+int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
+                 cudaStream_t st);
+int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
+                 int64_t* out, cudaStream_t st);
+
+constexpr int SIDX_CAP = 24576;  // doubles of index kept in shared memory (192 KB, 1 CTA per SM)
+constexpr int64_t TS_U = (int64_t)THREADS * K_UNIF;
+
+struct SmemLevels {
+  int k_smem;       // levels k >= k_smem are staged in shared memory (k_smem > levels: none)
+  int64_t base;     // idx offset of level k_smem
+  int64_t count;    // doubles staged
+};
+
+SmemLevels plan_smem_levels(const IndexDesc& d) {
+  SmemLevels s{d.levels + 1, 0, 0};
+  if (d.levels == 0) return s;
+  const int64_t end = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
+  for (int k = d.levels; k >= 1; --k) {
+    if (end - d.off[k] > SIDX_CAP) break;
+    s.k_smem = k;
+    s.base = d.off[k];
+    s.count = end - d.off[k];
+  }
+  return s;
+}
+
+__device__ __forceinline__ int count_lt16_smem(const double* p, double x) {
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < 16; i += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(p + i);
+    c += (v.x < x) ? 1 : 0;
+    c += (v.y < x) ? 1 : 0;
+  }
+  return c;
+}
+
+// index_lower_bound with the top levels in shared memory
+__device__ __forceinline__ int64_t search_sm(const double* __restrict__ W, const double* __restrict__ idx,
+                                             const double* sidx, const IndexDesc& d, const SmemLevels& sl,
+                                             double x) {
+  int64_t b = 0;
+  for (int k = d.levels; k >= 1; --k) {
+    int c;
+    if (k >= sl.k_smem) c = count_lt16_smem(sidx + (d.off[k] - sl.base) + FANOUT * b, x);
+    else c = count_lt16(idx + d.off[k] + FANOUT * b, x);
+    const int64_t valid = d.n[k] - FANOUT * b;
+    if (c >= valid) c = (int)valid - 1;
+    b = FANOUT * b + c;
+  }
+  const int64_t j0 = FANOUT * b;
+  const int64_t valid = d.n[0] - j0;
+  int c;
+  if (valid >= FANOUT) {
+    c = count_lt16(W + j0, x);
+  } else {
+    c = 0;
+    for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x) ? 1 : 0;
+  }
+  if (c >= valid) c = (int)valid - 1;
+  return j0 + c;
+}
+
+// four independent searches in lock-step: the level loop is outside, so the
+// four lines of a level are in flight together
+__device__ __forceinline__ void search4_sm(const double* __restrict__ W, const double* __restrict__ idx,
+                                           const double* sidx, const IndexDesc& d, const SmemLevels& sl,
+                                           const double x[4], int64_t r[4]) {
+  int64_t b[4] = {0, 0, 0, 0};
+  for (int k = d.levels; k >= 1; --k) {
+    int c[4];
+    if (k >= sl.k_smem) {
+      const double* base = sidx + (d.off[k] - sl.base);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] = count_lt16_smem(base + FANOUT * b[q], x[q]);
+    } else {
+      const double* base = idx + d.off[k];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] = count_lt16(base + FANOUT * b[q], x[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t valid = d.n[k] - FANOUT * b[q];
+      if (c[q] >= valid) c[q] = (int)valid - 1;
+      b[q] = FANOUT * b[q] + c[q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int64_t j0 = FANOUT * b[q];
+    const int64_t valid = d.n[0] - j0;
+    int c;
+    if (valid >= FANOUT) {
+      c = count_lt16(W + j0, x[q]);
+    } else {
+      c = 0;
+      for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
+    }
+    if (c >= valid) c = (int)valid - 1;
+    r[q] = j0 + c;
+  }
+}
+
+// Sense-free grid barrier for a cooperative launch (all CTAs co-resident).
+__device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t g = ld_acquire_u32(gen);
+    __threadfence();
+    if (atomicAdd(count, 1u) == gridDim.x - 1) {
+      *count = 0;
+      __threadfence();
+      st_release_u32(gen, g + 1);
+    } else {
+      while (ld_acquire_u32(gen) == g) __nanosleep(20);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ double chain_fold_f(double tau, double* s_g, double& Q, double& R) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double acc = 0.0;
+  Q = 0.0;
+#pragma unroll
+  for (int k = 0; k < LANES; ++k) {
+    if (lane == k) Q = acc;
+    acc = __dadd_rn(acc, __shfl_sync(FULL, tau, k));
+  }
+  if (lane == 0) s_g[warp] = acc;
+  __syncthreads();
+  double r = 0.0;
+  R = 0.0;
+#pragma unroll
+  for (int v = 0; v < WARPS; ++v) {
+    if (v == warp) R = r;
+    r = __dadd_rn(r, s_g[v]);
+  }
+  return r;
+}
+
+struct FusedArgs {
+  const double* W;
+  const double* idx;
+  IndexDesc d;
+  SmemLevels sl;
+  uint64_t k0, k1, offset;
+  uint64_t* offset_dev;  // optional device-resident stream position
+  const double* raw;     // optional supplied uniforms (n+1) instead of Philox draws
+  int64_t n;
+  double* U;      // optional
+  int64_t* out;
+  int32_t* status;
+  ScanWS ws;
+};
+
+__global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant__ FusedArgs a) {
+  extern __shared__ __align__(128) double sidx[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ double s_g[WARPS];
+  __shared__ double s_last[WARPS];
+  __shared__ double s_P, s_total;
+  __shared__ unsigned long long s_min;
+  __shared__ uint32_t s_flag;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t t = blockIdx.x;
+  const int64_t nt = gridDim.x;
+  const int64_t n = a.n;
+  uint32_t* bcount = &a.ws.hdr->bar_count;
+  uint32_t* bgen = &a.ws.hdr->bar_gen;
+
+  // 1. prefetch the top index levels (TMA bulk copy, overlaps step 2)
+  const uint32_t sbytes = (uint32_t)(a.sl.count * 8);
+  if (threadIdx.x == 0) {
+    s_min = 0x7FF0000000000000ULL;
+    s_flag = 0;
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, sbytes);
+    if (sbytes) bulk_g2s(sidx, a.idx + a.sl.base, sbytes, &bar);
+  }
+  const uint64_t offset = a.offset_dev ? *(volatile uint64_t*)a.offset_dev : a.offset;
+  __syncthreads();
+
+  // 2. draws, spacings, tile chain
+  const int64_t e0 = t * TS_U + (int64_t)(warp * LANES + lane) * K_UNIF;
+  double z[4];
+  if (a.raw) {  // uniforms supplied by a host stream
+#pragma unroll
+    for (int i = 0; i < 4; ++i) z[i] = (e0 + i <= n) ? neglog(a.raw[e0 + i]) : 0.0;
+  } else {
+    const uint64_t d0 = offset + (uint64_t)e0;
+    const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
+    const U64x4 v0 = philox_block(a.k0, a.k1, b0);
+    U64x4 v1 = v0;
+    if (b1 != b0) v1 = philox_block(a.k0, a.k1, b1);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint64_t dd = d0 + (uint64_t)i;
+      const uint64_t raw = ((dd >> 2) == b0) ? pick(v0, (int)(dd & 3)) : pick(v1, (int)(dd & 3));
+      z[i] = (e0 + i <= n) ? neglog(u01(raw)) : 0.0;
+    }
+  }
+  unsigned long long mn = 0x7FF0000000000000ULL;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (e0 + i <= n) mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
+  double sc[4];
+  sc[0] = z[0];
+#pragma unroll
+  for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+  atomicMin(&s_min, mn);
+  double Q, R;
+  const double A = chain_fold_f(sc[3], s_g, Q, R);
+  if (threadIdx.x == 0) {
+    st_relaxed_f64(&a.ws.agg[t], A);
+    st_relaxed_f64(&a.ws.incl[t], __longlong_as_double((long long)s_min));
+  }
+
+  // 3. one grid barrier, then the chained fold of the tile totals before t
+  grid_barrier(bcount, bgen);
+  if (a.offset_dev && t == 0 && threadIdx.x == 0) *a.offset_dev = offset + (uint64_t)(n + 1);
+  if (warp == 0) {
+    // lanes stage 32 totals at a time; lane 0 folds them in tile order
+    double P = 0.0, total = 0.0;
+    unsigned long long gmin = 0x7FF0000000000000ULL;
+    for (int64_t base = 0; base < nt; base += 32) {
+      const int64_t tt = base + lane;
+      const double v = (tt < nt) ? ld_relaxed_f64(&a.ws.agg[tt]) : 0.0;
+      const double m = (tt < nt) ? ld_relaxed_f64(&a.ws.incl[tt]) : __longlong_as_double(0x7FF0000000000000LL);
+      gmin = min(gmin, (unsigned long long)__double_as_longlong(m));
+      // fully unrolled: the 32 shuffles issue back to back and only the adds
+      // chain; tiles past nt contribute +0.0, which leaves the fold unchanged
+      double vk[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) vk[k] = __shfl_sync(FULL, v, k);
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        P = (base + k == t) ? total : P;
+        total = __dadd_rn(total, vk[k]);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) gmin = min(gmin, __shfl_xor_sync(FULL, gmin, o));
+    if (lane == 0) {
+      s_P = P;
+      s_total = total;
+      s_min = gmin;
+    }
+  }
+  __syncthreads();
+  const double P = s_P, total = s_total;
+  const double zmin = __longlong_as_double((long long)s_min);
+  const bool need = !(zmin > __dmul_rn(1e-14, total));
+
+  // 4. U in registers
+  double u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u[i] = __ddiv_rn(__dadd_rn(P, __dadd_rn(R, __dadd_rn(Q, sc[i]))), total);
+
+  if (need) {  // grid-uniform: the reference's exactness check (randkit.py:95-100)
+    double prev_lane = __shfl_up_sync(FULL, u[3], 1);
+    if (lane == 31) s_last[warp] = u[3];
+    __syncthreads();
+    if (lane == 0) prev_lane = (warp > 0) ? s_last[warp - 1] : ((t == 0) ? 0.0 : __ddiv_rn(P, total));
+    bool site = false;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t e = e0 + i;
+      if (e < n) {
+        const double pv = (i == 0) ? prev_lane : u[i - 1];
+        if (u[i] <= pv) {
+          site = true;
+          const uint32_t slot = atomicAdd(&a.ws.hdr->nsites, 1u);
+          if (slot < (uint32_t)SITE_CAP) a.ws.sites[slot] = (long long)e;
+        }
+        if (e == n - 1 && u[i] >= 1.0) {
+          site = true;
+          atomicOr(&a.ws.hdr->top, 1u);
+        }
+      }
+      if (e < n) a.U[e] = u[i];  // U must be in memory for the repair
+    }
+    (void)site;
+    grid_barrier(bcount, bgen);
+    const uint32_t nsites = *(volatile uint32_t*)&a.ws.hdr->nsites;
+    const uint32_t top = *(volatile uint32_t*)&a.ws.hdr->top;
+    if (nsites || top) {
+      if (t == 0 && threadIdx.x == 0) {
+        // the forward / backward nextafter passes of randkit.py:104-116,
+        // restricted to the recorded collapse sites (see drs_scan.cu)
+        long long* sites = a.ws.sites;
+        double* U = a.U;
+        if (nsites > (uint32_t)SITE_CAP) {
+          double lo = 0.0;
+          for (int64_t i = 0; i < n; ++i) {
+            double v = ld_relaxed_f64(U + i);
+            if (v <= lo) { v = nextafter(lo, 1.0); U[i] = v; }
+            lo = v;
+          }
+        } else {
+          for (uint32_t q = 1; q < nsites; ++q) {
+            const long long key = sites[q];
+            int b = (int)q - 1;
+            while (b >= 0 && sites[b] > key) { sites[b + 1] = sites[b]; --b; }
+            sites[b + 1] = key;
+          }
+          int64_t done_to = -1;
+          for (uint32_t q = 0; q < nsites; ++q) {
+            int64_t i = sites[q];
+            if (i <= done_to) continue;
+            double lo = (i == 0) ? 0.0 : ld_relaxed_f64(U + i - 1);
+            while (i < n) {
+              const double v = ld_relaxed_f64(U + i);
+              if (!(v <= lo)) break;
+              lo = nextafter(lo, 1.0);
+              U[i] = lo;
+              ++i;
+            }
+            done_to = i;
+          }
+        }
+        double hi = 1.0;
+        for (int64_t i = n - 1; i >= 0; --i) {
+          const double v = ld_relaxed_f64(U + i);
+          if (!(v >= hi)) break;
+          hi = nextafter(hi, 0.0);
+          U[i] = hi;
+        }
+        s_flag = 1;
+      }
+      grid_barrier(bcount, bgen);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (e0 + i < n) u[i] = ld_relaxed_f64(a.U + e0 + i);
+    }
+  }
+
+  // 5. search: 4 sorted u's per thread, top index levels in shared memory
+  mbar_wait(&bar, 0);
+  int64_t r[4];
+  search4_sm(a.W, a.idx, sidx, a.d, a.sl, u, r);
+
+  // 6. write back
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (e0 + i < n) {
+      a.out[e0 + i] = r[i];
+      if (a.U && !need) a.U[e0 + i] = u[i];
+    }
+  }
+  __syncthreads();
+  if (t == 0 && threadIdx.x == 0) {
+    // every CTA read the offset and the shared words before the last barrier
+    *a.status = s_flag ? DRS_ST_REPAIRED : 0;
+  }
+  if (need) {
+    grid_barrier(bcount, bgen);  // all reads of nsites/top done before the reset
+    if (t == 0 && threadIdx.x == 0) {
+      a.ws.hdr->nsites = 0;
+      a.ws.hdr->top = 0;
+    }
+  }
+}
+
+// binary_sampler with the top index levels staged in shared memory
+__global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restrict__ W,
+                                                          const double* __restrict__ idx, IndexDesc d,
+                                                          SmemLevels sl, uint64_t k0, uint64_t k1,
+                                                          uint64_t offset, uint64_t* offset_dev,
+                                                          int64_t N, int64_t* __restrict__ out) {
+  extern __shared__ __align__(128) double sidx[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t sbytes = (uint32_t)(sl.count * 8);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, sbytes);
+    if (sbytes) bulk_g2s(sidx, idx + sl.base, sbytes, &bar);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
+  const uint64_t off = offset_dev ? *(volatile uint64_t*)offset_dev : offset;
+  const uint64_t d0 = off + (uint64_t)base;
+  const uint64_t b0 = d0 >> 2;
+  U64x4 v{0, 0, 0, 0};
+  if (lane < 9) v = philox_block(k0, k1, b0 + (uint64_t)lane);
+  const uint64_t dd = d0 + (uint64_t)lane;
+  const int src = (int)((dd >> 2) - b0);
+  const uint64_t w0 = __shfl_sync(FULL, v.w0, src), w1 = __shfl_sync(FULL, v.w1, src);
+  const uint64_t w2 = __shfl_sync(FULL, v.w2, src), w3 = __shfl_sync(FULL, v.w3, src);
+  const int wi = (int)(dd & 3);
+  const uint64_t raw = wi == 0 ? w0 : (wi == 1 ? w1 : (wi == 2 ? w2 : w3));
+  mbar_wait(&bar, 0);
+  const int64_t i = base + lane;
+  if (i < N) out[i] = search_sm(W, idx, sidx, d, sl, u01(raw));
+}
+
+__global__ void k_advance_offset(uint64_t* p, uint64_t by) { *p += by; }
+
+static int g_coop_blocks = -1;
+
+static int coop_capacity() {
+  if (g_coop_blocks < 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_dac_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dac_fused, THREADS, SIDX_CAP * 8);
+    g_coop_blocks = sms * per;
+  }
+  return g_coop_blocks;
+}
+
+}  // namespace drs
+
+using namespace drs;
+
+namespace drs {
+int sorted_uniforms_from_launch(const double* raw, int64_t n, double* U, int32_t* status, void* ws,
+                                size_t ws_bytes, cudaStream_t st);
+
+static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
+                           uint64_t offset, uint64_t* offset_dev, const double* raw, int64_t N,
+                           double* U, int64_t* out, int32_t* status, int32_t mode, void* ws,
+                           size_t ws_bytes, cudaStream_t st) {
+  if (M < 1 || N < 1 || !W || !out || !status || !ws || !U) return DRS_ERR_ARG;
+  if (mode != DRS_DAC_AUTO && mode != DRS_DAC_MERGE && mode != DRS_DAC_SEARCH) return DRS_ERR_MODE;
+  if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
+  const IndexDesc d = make_index_desc(M);
+  if (d.levels > 0 && !idx) return DRS_ERR_ARG;
+  const int64_t nt = cdiv(N + 1, TS_U);
+  const bool merge = (mode == DRS_DAC_MERGE) || (mode == DRS_DAC_AUTO && M <= 16 * N);
+  if (!merge && nt <= coop_capacity() && nt <= ws_capacity_tiles(ws_bytes)) {
+    FusedArgs a;
+    a.W = W; a.idx = idx; a.d = d; a.sl = plan_smem_levels(d);
+    a.k0 = k0; a.k1 = k1; a.offset = offset; a.offset_dev = offset_dev; a.raw = raw;
+    a.n = N; a.U = U; a.out = out; a.status = status;
+    a.ws = carve_ws(ws, ws_bytes);
+    void* args[] = {&a};
+    const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3((unsigned)nt), dim3(THREADS),
+                                                      args, (size_t)SIDX_CAP * 8, st);
+    return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+  }
+  const int rc = raw ? sorted_uniforms_from_launch(raw, N, U, status, ws, ws_bytes, st)
+                     : sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
+  if (rc) return rc;
+  return merge ? launch_merge(W, M, U, N, out, st) : launch_index(W, idx, M, U, N, out, st);
+}
+}  // namespace drs
+
+extern "C" {
+
+int dr_sample_dac_from(const double* W, const double* idx, int64_t M, const double* raw, int64_t N,
+                       double* U, int64_t* out, int32_t* status, int32_t mode, void* ws,
+                       size_t ws_bytes, void* stream) {
+  if (!raw) return DRS_ERR_ARG;
+  return sample_dac_impl(W, idx, M, 0, 0, 0, nullptr, raw, N, U, out, status, mode, ws, ws_bytes,
+                         (cudaStream_t)stream);
+}
+
+int dr_sample_dac(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
+                  uint64_t offset, uint64_t* offset_dev, int64_t N, double* U, int64_t* out,
+                  int32_t* status, int32_t mode, void* ws, size_t ws_bytes, void* stream) {
+  return sample_dac_impl(W, idx, M, k0, k1, offset, offset_dev, nullptr, N, U, out, status, mode, ws,
+                         ws_bytes, (cudaStream_t)stream);
+}
+
+int dr_sample_ccf(const double* W, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,
+                  uint64_t* offset_dev, int64_t N, double* U, int64_t* out, int32_t* status, void* ws,
+                  size_t ws_bytes, void* stream) {
+  if (M < 1 || N < 1 || !W || !U || !out || !status || !ws) return DRS_ERR_ARG;
+  if ((uintptr_t)W & 15) return DRS_ERR_ALIGN;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
+  if (rc) return rc;
+  return launch_merge(W, M, U, N, out, st);
+}
+
+int dr_sample_binary_dev(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
+                      uint64_t offset, uint64_t* offset_dev, int64_t N, int64_t* out, void* stream) {
+  if (M < 1 || N < 0 || !W || (N > 0 && !out)) return DRS_ERR_ARG;
+  if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
+  if (N == 0) return DRS_OK;
+  const IndexDesc d = make_index_desc(M);
+  if (d.levels > 0 && !idx) return DRS_ERR_ARG;
+  const SmemLevels sl = plan_smem_levels(d);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sample_binary_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
+    attr = true;
+  }
+  k_sample_binary_sm<<<(unsigned)cdiv(N, 256), 256, (size_t)sl.count * 8, (cudaStream_t)stream>>>(
+      W, idx, d, sl, k0, k1, offset, offset_dev, N, out);
+  if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
+  if (offset_dev) k_advance_offset<<<1, 1, 0, (cudaStream_t)stream>>>(offset_dev, (uint64_t)N);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
+}  // extern "C"

@@ -203,7 +203,7 @@ __global__ void k_lower_bound_range(const double* __restrict__ W, int64_t lo, in
 }
 
 static bool g_merge_attr = false;
-static int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
+int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
                         cudaStream_t st) {
   const int smem = TW * 8 + UCH * 8;
   if (!g_merge_attr) {
@@ -224,7 +224,7 @@ int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st)
   return launch_rc();
 }
 
-static int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
+int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
                         int64_t* out, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
   k_match_index<<<(unsigned)cdiv(N, 256), 256, 0, st>>>(W, idx, d, u, N, out);

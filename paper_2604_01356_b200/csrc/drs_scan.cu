@@ -46,7 +46,7 @@ __host__ inline ScanWS carve(void* ws, size_t ws_bytes) {
 
 __global__ void k_ws_init(ScanHdr* h) {
   h->ticket = 0; h->done1 = 0; h->done2 = 0; h->epoch = 1;
-  h->status = 0; h->nsites = 0; h->top = 0;
+  h->status = 0; h->nsites = 0; h->top = 0; h->bar_count = 0; h->bar_gen = 0;
   h->zmin_bits = 0x7FF0000000000000ULL;
 }
 
@@ -75,7 +75,15 @@ __device__ __forceinline__ double chain_fold(double tau, double* s_g, double& Q,
 }
 
 // Decoupled look-back, executed by warp 0.  Returns the exclusive prefix P_t.
-__device__ double lookback(const ScanWS& ws, int64_t t, uint32_t ep, double A) {
+// The warp inspects 32 predecessors at a time; a window holding only
+// aggregates is stashed in shared memory and the walk continues further back
+// (up to LB_MAXW windows), so the inclusive frontier is never a bottleneck.
+// The prefix is always the left fold incl[k] + agg[k+1] + ... + agg[t-1]
+// from the nearest published inclusive k, which equals the chained value
+// incl[t-1] bit for bit whichever k was found.
+constexpr int LB_MAXW = 16;
+
+__device__ double lookback(const ScanWS& ws, int64_t t, uint32_t ep, double A, double* s_win) {
   const int lane = threadIdx.x & 31;
   if (t == 0) {
     const double I = __dadd_rn(0.0, A);
@@ -89,7 +97,8 @@ __device__ double lookback(const ScanWS& ws, int64_t t, uint32_t ep, double A) {
     st_relaxed_f64(&ws.agg[t], A);
     st_release_u32(&ws.flags[t], (ep << 2) | 1u);
   }
-  const int64_t base = t - 1;
+  int64_t base = t - 1;
+  int nw = 0;
   double P = 0.0;
   int spins = 0;
   while (true) {
@@ -112,9 +121,18 @@ __device__ double lookback(const ScanWS& ws, int64_t t, uint32_t ep, double A) {
         for (int k = j - 1; k >= 0; --k) P = __dadd_rn(P, __shfl_sync(FULL, val, k));
         break;
       }
+    } else if (avail_mask == FULL && nw < LB_MAXW) {
+      s_win[nw * 32 + lane] = ld_relaxed_f64(&ws.agg[tt]);
+      __syncwarp();
+      ++nw;
+      base -= 32;
+      spins = 0;
+      continue;
     }
     if (++spins > 4) __nanosleep(32);
   }
+  for (int w = nw - 1; w >= 0; --w)
+    for (int k = 31; k >= 0; --k) P = __dadd_rn(P, s_win[w * 32 + k]);
   const double I = __dadd_rn(P, A);
   if (lane == 0) {
     st_relaxed_f64(&ws.incl[t], I);
@@ -166,6 +184,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
   __shared__ double s_g[WARPS];
   __shared__ int64_t s_tile;
   __shared__ uint32_t s_ep;
+  __shared__ double s_win[LB_MAXW * 32];
   if (threadIdx.x == 0) {
     s_tile = (int64_t)atomicAdd(&ws.hdr->ticket, 1u);
     s_ep = *(volatile uint32_t*)&ws.hdr->epoch;
@@ -187,7 +206,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
   double Q, R;
   const double A = chain_fold(s, s_g, Q, R);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.hdr->status, (uint32_t)DRS_ST_INVALID_WEIGHT);
-  if (warp == 0) lookback(ws, t, ep, A);
+  if (warp == 0) lookback(ws, t, ep, A, s_win);
   pass1_finish(ws, ep);
 }
 
@@ -269,9 +288,11 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
 // Spacing sources: element e (0 <= e <= n) of the n+1 spacings.
 struct PhiloxSpacings {
   uint64_t k0, k1, offset;
-  // the K_UNIF = 4 consecutive spacings starting at e0 (e0 % 4 == 0)
+  const uint64_t* offset_dev;  // device-resident stream position (graph capture)
+  // the K_UNIF = 4 consecutive spacings starting at e0
   __device__ __forceinline__ void chunk4(int64_t e0, int64_t count, double z[4]) const {
-    const uint64_t d0 = offset + (uint64_t)e0;
+    const uint64_t off = offset_dev ? *(volatile const uint64_t*)offset_dev : offset;
+    const uint64_t d0 = off + (uint64_t)e0;
     const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
     const U64x4 v0 = philox_block(k0, k1, b0);
     U64x4 v1 = v0;
@@ -305,6 +326,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   __shared__ int64_t s_tile;
   __shared__ uint32_t s_ep;
   __shared__ unsigned long long s_min;
+  __shared__ double s_win[LB_MAXW * 32];
   if (threadIdx.x == 0) {
     s_tile = (int64_t)atomicAdd(&ws.hdr->ticket, 1u);
     s_ep = *(volatile uint32_t*)&ws.hdr->epoch;
@@ -329,7 +351,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   double Q, R;
   const double A = chain_fold(s, s_g, Q, R);  // contains __syncthreads
   if (threadIdx.x == 0) atomicMin(&ws.hdr->zmin_bits, s_min);
-  if (warp == 0) lookback(ws, t, ep, A);
+  if (warp == 0) lookback(ws, t, ep, A, s_win);
   pass1_finish(ws, ep);
 }
 
@@ -508,6 +530,9 @@ int64_t index_entries(int64_t M) {
   return d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
 }
 
+int64_t ws_capacity_tiles(size_t ws_bytes) { return ws_tile_capacity(ws_bytes); }
+ScanWS carve_ws(void* ws, size_t ws_bytes) { return carve(ws, ws_bytes); }
+
 template <class Src>
 static int sorted_impl(const Src& src, int64_t n, double* U, int32_t* status, void* ws,
                        size_t ws_bytes, cudaStream_t st) {
@@ -517,6 +542,22 @@ static int sorted_impl(const Src& src, int64_t n, double* U, int32_t* status, vo
   k_unif_pass1<Src><<<(unsigned)nt, THREADS, 0, st>>>(src, n, s);
   k_unif_pass2<Src><<<(unsigned)nt, THREADS, 0, st>>>(src, n, nt, s, U, status);
   return launch_rc();
+}
+
+int sorted_uniforms_launch(uint64_t k0, uint64_t k1, uint64_t offset, const uint64_t* offset_dev,
+                           int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes,
+                           cudaStream_t st) {
+  PhiloxSpacings src{k0, k1, offset, offset_dev};
+  const int rc = sorted_impl(src, n, U, status, ws, ws_bytes, st);
+  if (rc || !offset_dev) return rc;
+  k_advance_offset<<<1, 1, 0, st>>>(const_cast<uint64_t*>(offset_dev), (uint64_t)(n + 1));
+  return launch_rc();
+}
+
+int sorted_uniforms_from_launch(const double* raw, int64_t n, double* U, int32_t* status, void* ws,
+                                size_t ws_bytes, cudaStream_t st) {
+  ArraySpacings src{raw};
+  return sorted_impl(src, n, U, status, ws, ws_bytes, st);
 }
 
 }  // namespace drs
@@ -606,8 +647,7 @@ int dr_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t k, double* u,
 int dr_sorted_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, double* U,
                        int32_t* status, void* ws, size_t ws_bytes, void* stream) {
   if (n < 1 || !U || !status || !ws) return DRS_ERR_ARG;
-  PhiloxSpacings src{k0, k1, offset};
-  return sorted_impl(src, n, U, status, ws, ws_bytes, (cudaStream_t)stream);
+  return sorted_uniforms_launch(k0, k1, offset, nullptr, n, U, status, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int dr_sorted_uniforms_from(const double* raw, int64_t n, double* U, int32_t* status, void* ws,

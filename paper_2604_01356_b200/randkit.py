@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from ._tensors import empty_f64, status_word, to_device_f64
 
-__all__ = ["RngStream", "uniform_open", "sorted_uniforms"]
+__all__ = ["RngStream", "DeviceRngStream", "uniform_open", "sorted_uniforms"]
 
 
 class RngStream:
@@ -89,6 +89,41 @@ class RngStream:
 
     def __repr__(self):
         return f"RngStream(seed={self.seed}, substream={self._spawn_key})"
+
+
+class DeviceRngStream:
+    """An RngStream whose draw position lives in device memory.
+
+    The samplers read the position on the device and advance it there, so a
+    sampler call can be captured once in a CUDA graph and replayed with fresh
+    draws on every replay (the loop of a particle filter).  Same key
+    derivation and draw sequence as :class:`RngStream`; ``position`` reads
+    the device counter (synchronising).
+    """
+
+    __slots__ = ("seed", "_spawn_key", "_key", "offset_tensor")
+
+    def __init__(self, seed: int, _spawn_key: tuple[int, ...] = (), position: int = 0):
+        self.seed = int(seed)
+        self._spawn_key = tuple(int(k) for k in _spawn_key)
+        k = np.random.SeedSequence(self.seed, spawn_key=self._spawn_key).generate_state(2, np.uint64)
+        self._key = (int(k[0]), int(k[1]))
+        self.offset_tensor = torch.tensor([int(position)], dtype=torch.int64, device=_lib.device())
+
+    @property
+    def key(self) -> tuple[int, int]:
+        return self._key
+
+    @property
+    def position(self) -> int:
+        return int(self.offset_tensor.item())
+
+    @property
+    def draws(self) -> int:
+        return self.position
+
+    def __repr__(self):
+        return f"DeviceRngStream(seed={self.seed}, substream={self._spawn_key})"
 
 
 def uniform_open(stream: RngStream) -> float:

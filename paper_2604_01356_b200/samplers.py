@@ -26,7 +26,7 @@ import torch
 from . import _lib
 from ._tensors import empty_i64, is_device_tensor, read_status, status_word, to_device_f64
 from .cdf import WeightTable
-from .randkit import RngStream, sorted_uniforms_device
+from .randkit import DeviceRngStream, RngStream, sorted_uniforms_device
 
 __all__ = [
     "OpStats",
@@ -150,49 +150,100 @@ def dac_match(u, table: WeightTable, stats: OpStats | None = None, check: bool =
     return _match("dac", u, table, check, mode)
 
 
+def _stream_args(stream, n_draws):
+    """(k0, k1, offset, offset_dev pointer) for a Philox stream, advancing host streams."""
+    if isinstance(stream, DeviceRngStream):
+        return stream.key[0], stream.key[1], 0, stream.offset_tensor.data_ptr()
+    off = stream._take(n_draws)
+    return stream.key[0], stream.key[1], off, 0
+
+
 def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
-                   *, device: bool = False):
+                   *, device: bool = False, out=None):
     """n independent draws, each by a full-range search; draw order kept (samplers.py:238-252)."""
     _no_stats(stats, "binary_sampler")
     n = int(n)
     if n < 0:
         raise ValueError("negative dimensions are not allowed")
-    out = empty_i64(n)
+    out = empty_i64(n) if out is None else out
     if n:
-        L = _lib.lib()
-        s = _lib.stream_handle()
         W = table.device_cum
-        if isinstance(stream, RngStream):
-            off = stream._take(n)
-            rc = L.dr_sample_binary(W.data_ptr(), _ptr(table.device_index), table.size,
-                                    stream.key[0], stream.key[1], off, n, out.data_ptr(), s)
-            _lib.check(rc, "dr_sample_binary")
+        if isinstance(stream, (RngStream, DeviceRngStream)):
+            k0, k1, off, offd = _stream_args(stream, n)
+            rc = _lib.lib().dr_sample_binary_dev(W.data_ptr(), _ptr(table.device_index), table.size,
+                                                 k0, k1, off, offd, n, out.data_ptr(), _lib.stream_handle())
+            _lib.check(rc, "dr_sample_binary_dev")
         else:
             us, _ = to_device_f64(stream.uniforms(n))
             out = _lower_bounds(table, us)
     return out if device else out.cpu().numpy()
 
 
-def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto"):
+_status_cache: dict[int, torch.Tensor] = {}
+
+
+def _status_buf() -> torch.Tensor:
+    """A per-stream status word the kernels overwrite (no per-call zeroing)."""
+    s = _lib.stream_handle()
+    t = _status_cache.get(s)
+    if t is None:
+        t = torch.empty(1, dtype=torch.int32, device=_lib.device())
+        _status_cache[s] = t
+    return t
+
+
+def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None, U=None):
     _no_stats(stats, f"{kind}_sampler")
     n = int(n)
-    U = sorted_uniforms_device(stream, n)
-    out = _match(kind, U, table, check=False, mode=mode)
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    if n == 0 or (kind == "ccf" and not isinstance(stream, (RngStream, DeviceRngStream))):
+        U = sorted_uniforms_device(stream, n)
+        res = _match(kind, U, table, check=False, mode=mode)
+        return res if device else res.cpu().numpy()
+    L = _lib.lib()
+    out = empty_i64(n) if out is None else out
+    U = torch.empty(n, dtype=torch.float64, device=_lib.device()) if U is None else U
+    st = _status_buf()
+    ws, wsb = _lib.workspace(L.dr_workspace_bytes(_lib.OP_SORTED, 0, n, 0))
+    W = table.device_cum
+    s = _lib.stream_handle()
+    if not isinstance(stream, (RngStream, DeviceRngStream)):
+        # duck-typed host stream: its n+1 uniforms feed the same fused kernel
+        raw, _ = to_device_f64(stream.uniforms(n + 1))
+        rc = L.dr_sample_dac_from(W.data_ptr(), _ptr(table.device_index), table.size, raw.data_ptr(), n,
+                                  U.data_ptr(), out.data_ptr(), st.data_ptr(), _lib.DAC_MODES[mode], ws, wsb, s)
+        _lib.check(rc, "dr_sample_dac_from")
+        return out if device else out.cpu().numpy()
+    k0, k1, off, offd = _stream_args(stream, n + 1)
+    if kind == "ccf":
+        rc = L.dr_sample_ccf(W.data_ptr(), table.size, k0, k1, off, offd, n, U.data_ptr(), out.data_ptr(),
+                             st.data_ptr(), ws, wsb, s)
+    else:
+        rc = L.dr_sample_dac(W.data_ptr(), _ptr(table.device_index), table.size, k0, k1, off, offd, n,
+                             U.data_ptr(), out.data_ptr(), st.data_ptr(), _lib.DAC_MODES[mode], ws, wsb, s)
+    _lib.check(rc, f"dr_sample_{kind}")
     return out if device else out.cpu().numpy()
 
 
 def ccf_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
-                *, device: bool = False):
+                *, device: bool = False, out=None, uniforms_out=None):
     """Sorted uniforms + streaming merge: multinomial(w, n) in O(M + N) (samplers.py:255-259)."""
-    return _sorted_sampler("ccf", table, n, stream, stats, device)
+    return _sorted_sampler("ccf", table, n, stream, stats, device, out=out, U=uniforms_out)
 
 
 def dac_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
-                *, device: bool = False, mode: str = "auto"):
-    """Sorted uniforms + divide-and-conquer (samplers.py:262-266)."""
+                *, device: bool = False, mode: str = "auto", out=None, uniforms_out=None):
+    """Sorted uniforms + divide-and-conquer (samplers.py:262-266).
+
+    With a Philox stream this is one library call (``dr_sample_dac``): for
+    N+1 <= 1024 x (co-resident CTAs) a single cooperative kernel generates,
+    scans and normalises the uniforms in registers and searches them.
+    ``out`` / ``uniforms_out`` take preallocated CUDA buffers.
+    """
     if mode not in _lib.DAC_MODES:
         raise ValueError(f"unknown mode {mode!r}")
-    return _sorted_sampler("dac", table, n, stream, stats, device, mode)
+    return _sorted_sampler("dac", table, n, stream, stats, device, mode, out=out, U=uniforms_out)
 
 
 def warm_kernels() -> None:

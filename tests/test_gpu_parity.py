@@ -312,3 +312,75 @@ def test_sharded_single_gpu_emulation(drs, orc):
         k0, k1 = orc.key_of(2005)
         Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
         np.testing.assert_array_equal(full.cpu().numpy(), orc.match("dac", Wo, Uo))
+
+
+# ------------------------------------------------------------- fused sampler
+@pytest.mark.parametrize("M,N", [(1 << 16, 1), (1 << 16, 1023), (1 << 20, 4095), (1 << 26, 1 << 16),
+                                 (1 << 22, 150000), (3000000, 100001)])
+def test_fused_dac_equals_two_pass_and_oracle(drs, orc, M, N):
+    rng = np.random.default_rng(M ^ N)
+    w = np.exp(4 * rng.standard_normal(M))
+    w[rng.random(M) < 0.05] = 0.0
+    t = drs.build_weight_table(w)
+    fused = drs.dac_sampler(t, N, drs.RngStream(5, (N,)), mode="search", device=True)
+    twopass = drs.dac_sampler(t, N, drs.RngStream(5, (N,)), mode="merge", device=True)
+    np.testing.assert_array_equal(fused.cpu().numpy(), twopass.cpu().numpy())
+    k0, k1 = orc.key_of(5, (N,))
+    Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+    np.testing.assert_array_equal(fused.cpu().numpy(), orc.match("dac", t.cum, Uo))
+    U = torch.empty(N, dtype=torch.float64, device="cuda")
+    drs.dac_sampler(t, N, drs.RngStream(5, (N,)), mode="search", device=True, uniforms_out=U)
+    np.testing.assert_array_equal(U.cpu().numpy(), Uo)
+
+
+def test_fused_replay_and_repair(drs, orc, golden):
+    W = golden[f"tbl_cum_{int(golden['tbl_count']) - 1}"]
+    t = drs.WeightTable(W)
+    for i in range(int(golden["rp_count"])):
+        d = golden[f"rp_draws_{i}"]
+        n = d.shape[0] - 1
+        Uo, _ = orc.sorted_uniforms_from(d, n)
+        for mode in ("search", "merge"):
+            out = drs.dac_sampler(t, n, ReplayStream(d), mode=mode)
+            np.testing.assert_array_equal(out, orc.match("dac", W, Uo))
+    rng = np.random.default_rng(5)
+    d = rng.random(50001)
+    d[rng.random(50001) < 0.3] = 1 - 2.0 ** -53
+    Uo, st = orc.sorted_uniforms_from(d, 50000)
+    assert st & 0x20
+    U = torch.empty(50000, dtype=torch.float64, device="cuda")
+    out = drs.dac_sampler(t, 50000, ReplayStream(d), mode="search", uniforms_out=U)
+    np.testing.assert_array_equal(U.cpu().numpy(), Uo)
+    np.testing.assert_array_equal(out, orc.match("dac", W, Uo))
+
+
+def test_device_stream_graph_replay(drs):
+    w = np.exp(2 * np.random.default_rng(3).standard_normal(1 << 20))
+    t = drs.build_weight_table(w)
+    N = 4096
+    for kind, kw in (("dac", {"mode": "search"}), ("dac", {"mode": "merge"}), ("ccf", {}), ("binary", {})):
+        fn = {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}[kind]
+        host = drs.RngStream(11)
+        expect = [fn(t, N, host, **kw) for _ in range(3)]
+        ds = drs.DeviceRngStream(11)
+        out = torch.empty(N, dtype=torch.int64, device="cuda")
+        extra = {} if kind == "binary" else {"uniforms_out": torch.empty(N, dtype=torch.float64, device="cuda")}
+        fn(t, N, ds, device=True, out=out, **kw, **extra)  # warm (allocates workspaces)
+        ds.offset_tensor.zero_()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            fn(t, N, ds, device=True, out=out, **kw, **extra)  # workspace for this stream
+            ds.offset_tensor.zero_()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                fn(t, N, ds, device=True, out=out, **kw, **extra)
+        torch.cuda.current_stream().wait_stream(s)
+        ds.offset_tensor.zero_()
+        got = []
+        for _ in range(3):
+            g.replay()
+            got.append(out.cpu().numpy().copy())
+        for a, b in zip(got, expect):
+            np.testing.assert_array_equal(a, b)
+        assert ds.position == host.position
