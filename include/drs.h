@@ -31,6 +31,7 @@ extern "C" {
 #define DRS_SCAN_WARPS 8
 #define DRS_SCAN_K_TABLE 33 /* elements per lane chunk, table scans   */
 #define DRS_SCAN_K_UNIF 4   /* elements per lane chunk, spacing scans */
+#define DRS_SCAN_GROUP 256  /* tiles per group of the tile chain          */
 #define DRS_INDEX_FANOUT 16
 #define DRS_INDEX_MAX_LEVELS 12
 
@@ -64,8 +65,12 @@ extern "C" {
 
 const char *dr_version(void);
 const char *dr_strerror(int code);
-/* writes LANES, WARPS, K_TABLE, K_UNIF, FANOUT into g[0..4] */
-void dr_scan_geometry(int32_t g[5]);
+/* 1 when the device can dereference `p` at the same address (device memory,
+ * or pinned host memory under unified addressing, which the search kernels
+ * then write directly); 0 otherwise. */
+int dr_device_accessible(const void *p);
+/* writes LANES, WARPS, K_TABLE, K_UNIF, FANOUT, GROUP into g[0..5] */
+void dr_scan_geometry(int32_t g[6]);
 
 size_t dr_workspace_bytes(int op, int64_t M, int64_t N, int64_t B);
 int dr_workspace_init(void *ws, size_t ws_bytes, void *stream);
@@ -160,13 +165,15 @@ int dr_lower_bound_range(const double *W, int64_t lo, int64_t hi, double x, int6
                          void *stream);
 
 /* Batched independent filters (config 4; the reference's per-filter loop
- * over build_weight_table + dac_sampler): w[B][Mf] raw weights, keys[3B]
+ * over build_weight_table + dac_sampler): w[B][Mf] raw weights, keys[B][3]
  * (k0, k1, draw offset per filter) -> out[B][Nf]; U[B][Nf] and W[B][Mf]
- * are written when non-NULL.  One CTA per filter, table held in shared
- * memory.  status gets the OR over filters. */
-int dr_resample_batched(const double *w, int64_t B, int64_t Mf, int64_t Nf,
-                        const uint64_t *keys, double *W, double *U, int64_t *out,
-                        int32_t *status, void *stream);
+ * are written when non-NULL.  With advance != 0 each filter's draw offset
+ * is moved forward by Nf + 1 on the device (graph-replayable).  Persistent
+ * CTAs, weights staged in shared memory by TMA with L2 prefetch ahead.
+ * status gets the OR over filters.  Needs Mf*8 + (Nf+1)*8 + tables <= ~220 KB. */
+int dr_resample_batched(const double *w, int64_t B, int64_t Mf, int64_t Nf, uint64_t *keys,
+                        int32_t advance, double *W, double *U, int64_t *out, int32_t *status,
+                        void *stream);
 
 /* W-sharded table (config 5).
  * Step 1 on every rank: local chained scan of the rank's shard.

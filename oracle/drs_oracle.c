@@ -130,21 +130,27 @@ void drs_ref_neglog_array(const double *u, int64_t n, double *z) {
 }
 
 /* ------------------------------------------------------------------------ */
-/* The device's chained three-level scan.             */
+/* The device's chained scan.                        */
 /*   tile t = WARPS*LANES lane chunks of K consecutive elements              */
 /*   s      = serial inclusive sum inside the chunk (s = x0; s = s + xi)     */
 /*   Q      = serial fold of previous chunk totals inside the warp (from 0)  */
 /*   R      = serial fold of previous warp totals inside the tile (from 0)   */
-/*   P      = serial fold of previous tile totals (decoupled look-back)      */
-/*   S      = P + (R + (Q + s))                                              */
+/*   D      = serial fold of previous tile totals inside the group of        */
+/*            GROUP tiles (from 0)                                          */
+/*   C      = serial fold of previous group totals (from 0)                  */
+/*   S      = C + (D + (R + (Q + s)))                                        */
 /* Every group boundary value is the next group's base, so S is monotone    */
 /* for non-negative inputs and padding zeros are transparent.               */
 /* ------------------------------------------------------------------------ */
 void drs_ref_chain_scan(const double *x, int64_t n, int K, double *S, double *total) {
   const int64_t TS = (int64_t)DRS_REF_WARPS * DRS_REF_LANES * K;
   const int64_t nt = (n + TS - 1) / TS;
-  double P = 0.0;
+  double C = 0.0, D = 0.0;
   for (int64_t t = 0; t < nt; ++t) {
+    if (t > 0 && t % DRS_REF_GROUP == 0) {
+      C = C + D;
+      D = 0.0;
+    }
     double R = 0.0;
     for (int w = 0; w < DRS_REF_WARPS; ++w) {
       double Q = 0.0;
@@ -155,15 +161,15 @@ void drs_ref_chain_scan(const double *x, int64_t n, int K, double *S, double *to
           const int64_t j = base + i;
           const double xi = (j < n) ? x[j] : 0.0;
           s = (i == 0) ? xi : s + xi;
-          if (S && j < n) S[j] = P + (R + (Q + s));
+          if (S && j < n) S[j] = C + (D + (R + (Q + s)));
         }
         Q = Q + s;
       }
       R = R + Q;
     }
-    P = P + R;
+    D = D + R;
   }
-  if (total) *total = P;
+  if (total) *total = C + D;
 }
 
 /* build_weight_table (cdf.py:59-89) with the device association: validate,
@@ -490,6 +496,53 @@ double drs_port_throughput(int which, const double *W, int64_t M, int64_t N, int
     jobs[t].M = M; jobs[t].N = N; jobs[t].k0 = k0 + (uint64_t)t; jobs[t].k1 = k1;
     jobs[t].offset = 0;
     pthread_create(&th[t], NULL, port_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+  clock_gettime(CLOCK_MONOTONIC, &t1);
+  free(th);
+  free(jobs);
+  return (double)(t1.tv_sec - t0.tv_sec) + 1e-9 * (double)(t1.tv_nsec - t0.tv_nsec);
+}
+
+typedef struct {
+  const double *w;
+  int64_t f0, f1, Mf, Nf;
+  int reps;
+  uint64_t k0, k1;
+} batch_job;
+
+static void *batch_worker(void *arg) {
+  batch_job *j = (batch_job *)arg;
+  double *W = (double *)malloc(sizeof(double) * (size_t)j->Mf);
+  double *scratch = (double *)malloc(sizeof(double) * (size_t)(2 * j->Nf + 2));
+  int64_t *out = (int64_t *)malloc(sizeof(int64_t) * (size_t)(j->Nf > 0 ? j->Nf : 1));
+  for (int r = 0; r < j->reps; ++r)
+    for (int64_t f = j->f0; f < j->f1; ++f) {
+      drs_port_build_table(j->w + f * j->Mf, j->Mf, W);
+      drs_port_sampler(0, W, j->Mf, j->k0 + (uint64_t)f, j->k1, (uint64_t)r * (uint64_t)(j->Nf + 1), j->Nf,
+                       scratch, out);
+    }
+  free(W);
+  free(scratch);
+  free(out);
+  return NULL;
+}
+
+/* wall seconds for the reference's per-filter loop (build_weight_table +
+ * dac_sampler per filter, cdf.py:59-89 + samplers.py:262-266) over filters
+ * [0, B), `reps` times, the filters split into `threads` contiguous ranges */
+double drs_port_batched_throughput(const double *w, int64_t B, int64_t Mf, int64_t Nf, int threads,
+                                   int reps, uint64_t k0, uint64_t k1) {
+  if (threads < 1) threads = 1;
+  pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)threads);
+  batch_job *jobs = (batch_job *)malloc(sizeof(batch_job) * (size_t)threads);
+  struct timespec t0, t1;
+  clock_gettime(CLOCK_MONOTONIC, &t0);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t].w = w; jobs[t].Mf = Mf; jobs[t].Nf = Nf; jobs[t].reps = reps;
+    jobs[t].f0 = B * t / threads; jobs[t].f1 = B * (t + 1) / threads;
+    jobs[t].k0 = k0; jobs[t].k1 = k1;
+    pthread_create(&th[t], NULL, batch_worker, &jobs[t]);
   }
   for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
   clock_gettime(CLOCK_MONOTONIC, &t1);

@@ -39,6 +39,7 @@ extern "C" {
 #define DRS_REF_K_TABLE 33
 #define DRS_REF_K_UNIF 4
 #define DRS_REF_FANOUT 16
+#define DRS_REF_GROUP 256 /* tiles per group of the tile chain */
 
 /* status bits (same values as include/drs.h) */
 #define DRS_REF_ST_INVALID_WEIGHT 0x1
@@ -81,6 +82,8 @@ int drs_port_sampler(int which, const double *W, int64_t M, uint64_t k0, uint64_
                      uint64_t offset, int64_t N, double *scratch, int64_t *out);
 double drs_port_throughput(int which, const double *W, int64_t M, int64_t N, int threads,
                            int calls_per_thread, uint64_t k0, uint64_t k1);
+double drs_port_batched_throughput(const double *w, int64_t B, int64_t Mf, int64_t Nf, int threads,
+                                   int reps, uint64_t k0, uint64_t k1);
 
 #ifdef __cplusplus
 }

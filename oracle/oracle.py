@@ -47,6 +47,7 @@ _PROTOS = {
     "drs_port_sorted_uniforms": (_INT, [_U64, _U64, _U64, _I64, _P]),
     "drs_port_sampler": (_INT, [_INT, _P, _I64, _U64, _U64, _U64, _I64, _P, _P]),
     "drs_port_throughput": (_D, [_INT, _P, _I64, _I64, _INT, _INT, _U64, _U64]),
+    "drs_port_batched_throughput": (_D, [_P, _I64, _I64, _I64, _INT, _INT, _U64, _U64]),
 }
 
 _lib = None
@@ -227,3 +228,10 @@ def port_sampler(which, W, k0, k1, offset, N):
 def port_throughput(which, W, N, threads, calls, k0, k1):
     W = _f64(W)
     return float(lib().drs_port_throughput(SAMPLER_IDS[which], _p(W), W.size, int(N), int(threads), int(calls), k0, k1))
+
+
+def port_batched_throughput(w, Nf, threads, reps, k0, k1):
+    """Wall seconds of the reference's per-filter loop over the rows of w."""
+    w = _f64(w)
+    B, Mf = w.shape
+    return float(lib().drs_port_batched_throughput(_p(w), B, Mf, int(Nf), int(threads), int(reps), k0, k1))

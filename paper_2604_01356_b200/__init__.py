@@ -12,7 +12,7 @@ launch) and ``ShardedWeightTable`` / ``sharded_dac_sampler`` (one table split
 over several GPUs with a single all-gather of shard totals).
 """
 
-from .batched import resample_batched
+from .batched import BatchedStreams, resample_batched
 from .cdf import WeightTable, build_weight_table, upper_bound_search
 from .randkit import DeviceRngStream, RngStream, sorted_uniforms, uniform_open
 from .samplers import (
@@ -44,6 +44,7 @@ __all__ = [
     "dac_sampler",
     "warm_kernels",
     "resample_batched",
+    "BatchedStreams",
     "ShardedWeightTable",
     "build_sharded_table",
     "sharded_dac_sampler",

@@ -45,6 +45,7 @@ _dbl = ctypes.c_double
 _PROTOS = {
     "dr_version": (ctypes.c_char_p, []),
     "dr_strerror": (ctypes.c_char_p, [_int]),
+    "dr_device_accessible": (_int, [_c_void_p]),
     "dr_scan_geometry": (None, [_c_void_p]),
     "dr_workspace_bytes": (_size, [_int, _i64, _i64, _i64]),
     "dr_workspace_init": (_int, [_c_void_p, _size, _c_void_p]),
@@ -65,7 +66,7 @@ _PROTOS = {
     "dr_match_dac": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i32, _c_void_p]),
     "dr_check_sorted_open": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_lower_bound_range": (_int, [_c_void_p, _i64, _i64, _dbl, _c_void_p, _c_void_p]),
-    "dr_resample_batched": (_int, [_c_void_p, _i64, _i64, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
+    "dr_resample_batched": (_int, [_c_void_p, _i64, _i64, _i64, _c_void_p, _i32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "dr_shard_scan": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "dr_shard_finalize": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
     "dr_shard_range": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
@@ -111,6 +112,18 @@ def check(rc: int, what: str) -> None:
         raise RuntimeError(f"{what} failed: {msg} ({rc})")
 
 
+_accessible: dict[int, bool] = {}
+
+
+def device_accessible(ptr: int) -> bool:
+    """True when the device can dereference ``ptr`` itself (pinned host memory under UVA)."""
+    ok = _accessible.get(ptr)
+    if ok is None:
+        ok = bool(lib().dr_device_accessible(ptr))
+        _accessible[ptr] = ok
+    return ok
+
+
 def stream_handle() -> int:
     return torch.cuda.current_stream().cuda_stream
 
@@ -120,7 +133,7 @@ def device() -> torch.device:
 
 
 def scan_geometry() -> tuple[int, ...]:
-    g = (ctypes.c_int32 * 5)()
+    g = (ctypes.c_int32 * 6)()
     load_library().dr_scan_geometry(ctypes.cast(g, ctypes.c_void_p))
     return tuple(int(v) for v in g)
 

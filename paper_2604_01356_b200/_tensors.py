@@ -26,6 +26,11 @@ def to_device_f64(x) -> tuple[torch.Tensor, bool]:
             t = t.to(torch.float64).contiguous().clone()
         return t, False
     if isinstance(x, torch.Tensor):
+        if x.dtype == torch.float64 and x.is_contiguous() and x.is_pinned():
+            # pinned host input: asynchronous copy on the current stream
+            t = torch.empty(x.shape, dtype=torch.float64, device=_lib.device())
+            t.copy_(x, non_blocking=True)
+            return t, True
         x = x.detach().numpy()
     a = np.ascontiguousarray(x, dtype=np.float64)
     t = torch.empty(a.shape, dtype=torch.float64, device=_lib.device())
@@ -53,3 +58,24 @@ def read_status(st: torch.Tensor) -> int:
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     return t.cpu().numpy()
+
+
+def host_result_i64(n: int) -> torch.Tensor:
+    """A pinned (page-locked) host int64 buffer the kernels write directly.
+
+    Under unified addressing a pinned host allocation is device-accessible
+    at the same address, so the search kernels store the indices straight
+    into it over the host link (no separate device->host copy); the caller
+    synchronises the stream before reading.  ``_lib.device_accessible``
+    checks the address once per buffer.
+    """
+    t = torch.empty(int(n), dtype=torch.int64, pin_memory=True)
+    if t.numel() and not _lib.device_accessible(t.data_ptr()):
+        raise RuntimeError("pinned host buffer is not device-accessible (no unified addressing)")
+    return t
+
+
+def finish_host(t: torch.Tensor) -> np.ndarray:
+    """Wait for the stream that wrote ``t`` (pinned host memory) and hand it out as numpy."""
+    torch.cuda.current_stream().synchronize()
+    return t.numpy()

@@ -1,30 +1,67 @@
 // drs_batched.cu -- many independent filters in one launch (config 4).
 //
-// The reference resamples a batch of filters with a Python loop of
+// The reference resamples a bank of filters with a Python loop of
 // build_weight_table (cdf.py:59-89) + dac_sampler (samplers.py:262-266) per
-// filter.  Here one CTA owns one filter end to end: its raw weights arrive by
-// one TMA bulk copy, the table is scanned in shared memory with the same
-// chained association as dr_build_table (so W is bit-identical to the
-// single-filter path), the N_f+1 spacings are generated and scanned in
-// registers/shared memory exactly like dr_sorted_uniforms, and the N_f
-// lower bounds are found by bisection in shared memory.  Global traffic is
-// the raw weights once plus U and the indices.  Filters shard across GPUs
-// with no collective (the caller slices w/keys/out by filter).
+// filter.  Here one thread-block CLUSTER owns one filter, one CTA per table
+// tile of the chained scan (THREADS x K_TABLE = 8448 weights; M_f = 16384 is
+// a 2-CTA cluster):
+//
+//   * CTA r stages its tile of w_f in shared memory with one TMA bulk copy
+//     (~66 KB, so three CTAs share an SM and one CTA's copy overlaps the
+//     others' compute);
+//   * while the copy is in flight it generates and scans the N_f + 1 Philox
+//     spacings (they do not depend on w; every CTA of the cluster derives the
+//     same U, exactly as dr_sorted_uniforms does);
+//   * ONE sweep over the tile: each lane folds its K_TABLE-element chunk
+//     serially (validating from the high words in the integer pipe), writes
+//     the chunk-local prefix s2 in place, and the CTA folds lane and warp
+//     totals (Q, R) -- the chained association of dr_build_table, so W is
+//     bit-identical to the single-filter path;
+//   * the tile totals A_r are exchanged through distributed shared memory
+//     (st.shared::cluster + one cluster barrier); every CTA then folds the
+//     tile prefixes P_r and the filter total T in tile order;
+//   * CTA r answers exactly the draws u with W_end(r-1) < u <= W_end(r),
+//     W_end(r) = min(P_{r+1} / T, 1) being W at the tile's last entry, by
+//     bisection over its tile whose probes form
+//     W_j = min((P_r + (R + (Q + s2_j))) / T, 1) on the fly (~13 divisions
+//     per draw instead of one per weight; all of W only on request).
+// Global traffic per filter: w_f once, U and the indices (+ W on request).
+// The (k0, k1, offset) stream keys are read on the device and, with
+// `advance`, moved forward by N_f + 1 there (graph-replayable).  Filters
+// shard across GPUs with no collective.
 #include "drs_common.cuh"
 
 namespace drs {
 
 constexpr int64_t TS_TABLE = (int64_t)THREADS * K_TABLE;
 constexpr int64_t TS_UNIF = (int64_t)THREADS * K_UNIF;
-constexpr int MAX_TABLE_TILES = 3;  // Mf <= 25344 (shared memory bound)
+constexpr int MAX_TT = 8;  // table tiles per filter = cluster size (portable limit)
+constexpr int MAX_UT = 8;  // uniform tiles per filter
 
-__device__ __forceinline__ double chain_fold_b(double tau, double* s_g, double& Q, double& R) {
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// store v into the shared-memory word `local` of CTA `rank` of this cluster
+__device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, double v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+}
+
+// the chained in-tile fold of dr_build_table / dr_sorted_uniforms
+__device__ __forceinline__ double tile_fold(double tau, double* s_g, double& Q, double& R) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double acc = 0.0;
   Q = 0.0;
 #pragma unroll
   for (int k = 0; k < LANES; ++k) {
-    if (lane == k) Q = acc;
+    Q = (lane == k) ? acc : Q;
     acc = __dadd_rn(acc, __shfl_sync(FULL, tau, k));
   }
   if (lane == 0) s_g[warp] = acc;
@@ -32,169 +69,255 @@ __device__ __forceinline__ double chain_fold_b(double tau, double* s_g, double& 
   double r = 0.0;
   R = 0.0;
 #pragma unroll
-  for (int v = 0; v < WARPS; ++v) {
-    if (v == warp) R = r;
-    r = __dadd_rn(r, s_g[v]);
+  for (int q = 0; q < WARPS; ++q) {
+    R = (q == warp) ? r : R;
+    r = __dadd_rn(r, s_g[q]);
   }
-  __syncthreads();  // s_g is reused by the next tile
   return r;
 }
 
-__device__ __forceinline__ int smem_lb(const double* a, int n, double x) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int m = (lo + hi) >> 1;
-    if (a[m] < x) lo = m + 1;
-    else hi = m;
-  }
-  return lo;
+// valid weight <=> 0 <= x < inf (-0.0 included, NaN excluded); screened from
+// the high word: any sign bit (exact re-check follows) or an all-ones exponent
+__device__ __forceinline__ void track_hi(double x, uint32_t& any_sign, uint32_t& max_mag) {
+  const uint32_t hi = (uint32_t)__double2hiint(x);
+  any_sign |= hi;
+  max_mag = max(max_mag, hi & 0x7FFFFFFFu);
 }
 
-__global__ void __launch_bounds__(THREADS, 1)
-    k_resample_batched(const double* __restrict__ w, int64_t Mf, int64_t Nf,
-                       const uint64_t* __restrict__ keys, double* __restrict__ Wout,
-                       double* __restrict__ Uout, int64_t* __restrict__ out, int32_t* status) {
+struct BatchedArgs {
+  const double* w;
+  int64_t B, Mf, Nf;
+  uint64_t* keys;  // [B][3] = k0, k1, draw offset
+  int advance;     // move keys[f][2] forward by Nf + 1 on the device
+  double* Wout;    // optional [B][Mf]
+  double* Uout;    // optional [B][Nf]
+  int64_t* out;    // [B][Nf]
+  int32_t* status;
+  int ntt, ntu;
+};
+
+__global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ double s_g[WARPS];
+  __shared__ double s_g[WARPS];   // warp totals of the table tile
+  __shared__ double s_R[WARPS];   // warp bases R of the table tile
+  __shared__ double s_gu[WARPS];  // warp totals of a uniform tile
+  __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
+  __shared__ double s_Au[MAX_UT];
   __shared__ unsigned long long s_min;
   __shared__ int s_bad;
-  const int64_t f = blockIdx.x;
-  const int ntt = (int)cdiv(Mf, TS_TABLE);
-  const int64_t padM = (int64_t)ntt * TS_TABLE;
-  double* sw = sm;
-  double* su = sm + padM;  // Nf + 1 scanned spacings, then U
+  __shared__ int s_range[2];
+  const int64_t Mf = a.Mf, Nf = a.Nf, ne = Nf + 1;
+  const int r = (int)cluster_rank();
+  const int64_t f = blockIdx.x / a.ntt;
+  const int64_t j0 = (int64_t)r * TS_TABLE;  // first weight of this tile
+  const int len = (int)((Mf - j0) < TS_TABLE ? (Mf - j0) : TS_TABLE);
+  double* sw = sm;             // [TS_TABLE] raw w, then chunk-local prefixes s2
+  double* sQ = sw + TS_TABLE;  // [THREADS] lane-chunk bases Q
+  double* su = sQ + THREADS;   // [ne] inner sums, then U
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* wf = w + f * Mf;
+  const double* wt = a.w + f * Mf + j0;
+  const bool tma = ((((uintptr_t)wt) | ((uintptr_t)len * 8)) & 15) == 0;
 
-  // ---- stage the filter's raw weights (TMA bulk copy when 16-byte aligned)
-  const bool aligned = (((uintptr_t)wf) & 15) == 0;
-  const int64_t bulk = aligned ? (Mf & ~(int64_t)1) : 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
-    mbar_expect_tx(&bar, (uint32_t)(bulk * 8));
-    if (bulk > 0) bulk_g2s(sw, wf, (uint32_t)(bulk * 8), &bar);
+    if (tma) {
+      mbar_expect_tx(&bar, (uint32_t)len * 8u);
+      bulk_g2s(sw, wt, (uint32_t)len * 8u, &bar);
+    }
     s_min = 0x7FF0000000000000ULL;
     s_bad = 0;
   }
-  for (int64_t i = bulk + threadIdx.x; i < padM; i += THREADS) sw[i] = (i < Mf) ? wf[i] : 0.0;
+  if (!tma)
+    for (int i = threadIdx.x; i < len; i += THREADS) sw[i] = wt[i];
+  for (int i = len + threadIdx.x; i < TS_TABLE; i += THREADS) sw[i] = 0.0;  // tile padding
+  const uint64_t k0 = a.keys[3 * f], k1 = a.keys[3 * f + 1], off = a.keys[3 * f + 2];
   __syncthreads();
-  mbar_wait(&bar, 0);
+  // first half of a split cluster barrier: peers may store into this CTA's
+  // shared memory only once every CTA of the cluster is running
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
-  // ---- table: sweep 1 (tile totals and the chained tile prefixes)
-  double Pt[MAX_TABLE_TILES];
-  double P = 0.0;
-  bool bad = false;
-  for (int t = 0; t < ntt; ++t) {
-    const double* chunk = sw + t * TS_TABLE + (warp * LANES + lane) * K_TABLE;
-    double s = chunk[0];
-    bad |= !(s >= 0.0 && s < dinf());
+  // ---- 1. spacings and sorted uniforms, while the weights are in flight
+  if (Nf > 0) {
+    unsigned long long mn = 0x7FF0000000000000ULL;
+    for (int t = 0; t < a.ntu; ++t) {
+      const int64_t e0 = t * TS_UNIF + (int64_t)threadIdx.x * K_UNIF;
+      double z[4] = {0.0, 0.0, 0.0, 0.0};
+      if (e0 < ne) {
+        const uint64_t d0 = off + (uint64_t)e0;
+        const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
+        const U64x4 v0 = philox_block(k0, k1, b0);
+        U64x4 v1 = v0;
+        if (b1 != b0) v1 = philox_block(k0, k1, b1);
 #pragma unroll
-    for (int i = 1; i < K_TABLE; ++i) {
-      const double x = chunk[i];
-      bad |= !(x >= 0.0 && x < dinf());
-      s = __dadd_rn(s, x);
+        for (int i = 0; i < 4; ++i) {
+          const uint64_t dd = d0 + (uint64_t)i;
+          const uint64_t raw = ((dd >> 2) == b0) ? pick(v0, (int)(dd & 3)) : pick(v1, (int)(dd & 3));
+          if (e0 + i < ne) {
+            z[i] = neglog(u01(raw));
+            mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
+          }
+        }
+      }
+      double sc[4];
+      sc[0] = z[0];
+#pragma unroll
+      for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+      double Q, R;
+      const double A = tile_fold(sc[3], s_gu, Q, R);
+      if (threadIdx.x == 0) s_Au[t] = A;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (e0 + i < ne) su[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
+      __syncthreads();  // s_gu reuse
     }
-    double Q, R;
-    const double A = chain_fold_b(s, s_g, Q, R);
-    Pt[t] = P;
-    P = __dadd_rn(P, A);
-  }
-  const double T = P;
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(status, DRS_ST_INVALID_WEIGHT);
-  if (threadIdx.x == 0) {
-    int st = 0;
-    if (T == 0.0) st |= DRS_ST_DEGENERATE;
-    if (!(T < dinf())) st |= DRS_ST_ACCUM_OVERFLOW;
-    if (st) atomicOr(status, st);
-  }
-  // ---- table: sweep 2 (W in place)
-  for (int t = 0; t < ntt; ++t) {
-    double* chunk = sw + t * TS_TABLE + (warp * LANES + lane) * K_TABLE;
-    double s = chunk[0];
+    if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
+    double Pu[MAX_UT];
+    double total = 0.0;
 #pragma unroll
-    for (int i = 1; i < K_TABLE; ++i) s = __dadd_rn(s, chunk[i]);
-    double Q, R;
-    chain_fold_b(s, s_g, Q, R);
-    const int64_t jb = t * TS_TABLE + (warp * LANES + lane) * K_TABLE;
-    double s2 = 0.0;
+    for (int t = 0; t < MAX_UT; ++t) {
+      Pu[t] = total;
+      if (t < a.ntu) total = __dadd_rn(total, s_Au[t]);
+    }
+    for (int64_t i = threadIdx.x; i < Nf; i += THREADS) {
+      const int t = (int)(i / TS_UNIF);
+      double p = Pu[0];
+#pragma unroll
+      for (int q = 1; q < MAX_UT; ++q) p = (q == t) ? Pu[q] : p;
+      su[i] = __ddiv_rn(__dadd_rn(p, su[i]), total);
+    }
+    __syncthreads();
+    const double zmin = __longlong_as_double((long long)s_min);
+    if (!(zmin > __dmul_rn(1e-14, total)) && threadIdx.x == 0) {
+      // the exactness check and repair of randkit.py:95-116, serially: rare, Nf small
+      bool b2 = (su[0] <= 0.0) || (su[Nf - 1] >= 1.0);
+      for (int64_t i = 1; !b2 && i < Nf; ++i) b2 = !(__dsub_rn(su[i], su[i - 1]) > 0.0);
+      if (b2) {
+        double lo = 0.0;
+        for (int64_t i = 0; i < Nf; ++i) {
+          if (su[i] <= lo) su[i] = nextafter(lo, 1.0);
+          lo = su[i];
+        }
+        double hi = 1.0;
+        for (int64_t i = Nf - 1; i >= 0; --i) {
+          if (su[i] >= hi) su[i] = nextafter(hi, 0.0);
+          hi = su[i];
+        }
+        if (r == 0) atomicOr(a.status, DRS_ST_REPAIRED);
+      }
+    }
+  }
+
+  // ---- 2. the table sweep over this CTA's tile
+  if (tma) mbar_wait(&bar, 0);
+  uint32_t any_sign = 0, max_mag = 0;
+  const int c0 = threadIdx.x * K_TABLE;
+  double* chunk = sw + c0;
+  double s = 0.0;
+  if (c0 + K_TABLE <= len) {
 #pragma unroll
     for (int i = 0; i < K_TABLE; ++i) {
       const double x = chunk[i];
-      s2 = (i == 0) ? x : __dadd_rn(s2, x);
-      const double S = __dadd_rn(Pt[t], __dadd_rn(R, __dadd_rn(Q, s2)));
-      double v = fmin(__ddiv_rn(S, T), 1.0);
-      if (jb + i == Mf - 1) v = 1.0;
-      chunk[i] = v;
+      track_hi(x, any_sign, max_mag);
+      s = (i == 0) ? x : __dadd_rn(s, x);
+      chunk[i] = s;
     }
+  } else {
+#pragma unroll
+    for (int i = 0; i < K_TABLE; ++i) {
+      const double x = chunk[i];
+      track_hi(x, any_sign, max_mag);
+      s = (i == 0) ? x : __dadd_rn(s, x);
+      if (c0 + i < len) chunk[i] = s;
+    }
+  }
+  bool bad = max_mag >= 0x7FF00000u;  // inf or NaN
+  if (any_sign & 0x80000000u)         // a sign bit: re-check the raw weights (-0.0 is valid)
+    for (int i = 0; i < K_TABLE && c0 + i < len; ++i) bad |= !(wt[c0 + i] >= 0.0);
+  double Q, R;
+  const double A = tile_fold(s, s_g, Q, R);
+  sQ[threadIdx.x] = Q;
+  if (lane == 0) s_R[warp] = R;
+  if (bad) s_bad = 1;
+
+  // ---- 3. exchange the tile totals through distributed shared memory
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  if (threadIdx.x == 0)
+    for (int q = 0; q < a.ntt; ++q) st_cluster_f64(&s_A[r], (uint32_t)q, A);
+  cluster_sync_all();  // also the CTA barrier for sQ / s_R / s_bad / su
+  double Pr = 0.0, T = 0.0;
+  for (int q = 0; q < a.ntt; ++q) {
+    if (q == r) Pr = T;
+    T = __dadd_rn(T, s_A[q]);
+  }
+  const double Pnext = __dadd_rn(Pr, s_A[r]);  // == S at the tile's last entry
+  if (threadIdx.x == 0) {
+    int st = s_bad ? DRS_ST_INVALID_WEIGHT : 0;
+    if (r == 0) {
+      if (T == 0.0) st |= DRS_ST_DEGENERATE;
+      if (!(T < dinf())) st |= DRS_ST_ACCUM_OVERFLOW;
+      if (a.advance && Nf > 0) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every CTA has read it
+    }
+    if (st) atomicOr(a.status, st);
   }
 
-  // ---- sorted uniforms: Nf+1 spacings, chained scan over 1024-element tiles
-  const uint64_t k0 = keys[3 * f], k1 = keys[3 * f + 1], off = keys[3 * f + 2];
-  const int64_t ne = Nf + 1;
-  const int ntu = (int)cdiv(ne, TS_UNIF);
-  double Pu = 0.0;
-  unsigned long long mn = 0x7FF0000000000000ULL;
-  for (int t = 0; t < ntu; ++t) {
-    const int64_t e0 = t * TS_UNIF + (int64_t)(warp * LANES + lane) * K_UNIF;
-    const uint64_t d0 = off + (uint64_t)e0;
-    const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
-    const U64x4 v0 = philox_block(k0, k1, b0);
-    U64x4 v1 = v0;
-    if (b1 != b0) v1 = philox_block(k0, k1, b1);
-    double z[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint64_t dd = d0 + (uint64_t)i;
-      const uint64_t raw = ((dd >> 2) == b0) ? pick(v0, (int)(dd & 3)) : pick(v1, (int)(dd & 3));
-      z[i] = (e0 + i < ne) ? neglog(u01(raw)) : 0.0;
-      if (e0 + i < ne) mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
+  // ---- 4. the draws that land in this tile, by bisection on the unnormalised
+  // prefix: W_j < u  <=>  fl(S_j / T) < u  <=>  S_j < s*(u), where s*(u) is
+  // the least double s with fl(s / T) >= u (division is monotone in s), so the
+  // probes need no division and no clamp (the pinned last weight, W = 1 >= u,
+  // is never a probe of a lower-bound bisection: m < hi always).
+  if (Nf > 0) {
+    // u in (W_end(r-1), W_end(r)]; W_end(r-1) = min(P_r / T, 1); the last tile takes the rest
+    if (warp < 2) {
+      const bool first = (warp == 0);
+      int v;
+      if (first ? (r == 0) : (r == a.ntt - 1)) {
+        v = first ? 0 : (int)Nf;
+      } else {
+        const double key = fmin(__ddiv_rn(first ? Pr : Pnext, T), 1.0);
+        int lo = 0, hi = (int)Nf;  // #(su[i] <= key): 32-ary narrowing
+        while (hi - lo > 32) {
+          const int step = (hi - lo + 31) / 32;
+          const int p = lo + (lane + 1) * step - 1;
+          const int cnt = __popc(__ballot_sync(FULL, p < hi && su[p] <= key));
+          const int nhi = lo + (cnt + 1) * step - 1;
+          lo += cnt * step;
+          hi = nhi < hi ? nhi : hi;
+        }
+        v = lo + __popc(__ballot_sync(FULL, lo + lane < hi && su[lo + lane] <= key));
+      }
+      if (lane == 0) s_range[warp] = v;
     }
-    double sc[4];
-    sc[0] = z[0];
-#pragma unroll
-    for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
-    double Q, R;
-    const double A = chain_fold_b(sc[3], s_g, Q, R);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (e0 + i < ne) su[e0 + i] = __dadd_rn(Pu, __dadd_rn(R, __dadd_rn(Q, sc[i])));
-    Pu = __dadd_rn(Pu, A);
-  }
-  atomicMin(&s_min, mn);
-  __syncthreads();
-  const double total = Pu;
-  for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = __ddiv_rn(su[i], total);
-  __syncthreads();
-  const double zmin = __longlong_as_double((long long)s_min);
-  if (!(zmin > __dmul_rn(1e-14, total)) && threadIdx.x == 0 && Nf > 0) {
-    // exact check and repair (randkit.py:95-116), serial: rare and Nf is small
-    bool b2 = (su[0] <= 0.0) || (su[Nf - 1] >= 1.0);
-    for (int64_t i = 1; !b2 && i < Nf; ++i) b2 = !(__dsub_rn(su[i], su[i - 1]) > 0.0);
-    if (b2) {
-      double lo = 0.0;
-      for (int64_t i = 0; i < Nf; ++i) {
-        if (su[i] <= lo) su[i] = nextafter(lo, 1.0);
-        lo = su[i];
+    __syncthreads();
+    const int ib = s_range[0], ie = s_range[1];
+    for (int i = ib + threadIdx.x; i < ie; i += THREADS) {
+      const double x = su[i];
+      // s*(x): start at fl(x T), step by ulps (one or two divisions in practice)
+      double sx = __dmul_rn(x, T);
+      if (__ddiv_rn(sx, T) >= x) {
+        for (double p = nextafter(sx, -dinf()); __ddiv_rn(p, T) >= x; p = nextafter(p, -dinf())) sx = p;
+      } else {
+        do sx = nextafter(sx, dinf()); while (__ddiv_rn(sx, T) < x);
       }
-      double hi = 1.0;
-      for (int64_t i = Nf - 1; i >= 0; --i) {
-        if (su[i] >= hi) su[i] = nextafter(hi, 0.0);
-        hi = su[i];
+      int lo = 0, hi = len - 1;
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        const int c = m / K_TABLE;
+        const double S = __dadd_rn(Pr, __dadd_rn(s_R[c >> 5], __dadd_rn(sQ[c], sw[m])));
+        if (S < sx) lo = m + 1;
+        else hi = m;
       }
-      atomicOr(status, DRS_ST_REPAIRED);
+      a.out[f * Nf + i] = j0 + lo;
+      if (a.Uout) a.Uout[f * Nf + i] = x;
     }
   }
-  __syncthreads();
-
-  // ---- match (bisection in shared memory) and write back
-  for (int64_t i = threadIdx.x; i < Nf; i += THREADS) {
-    const double x = su[i];
-    out[f * Nf + i] = smem_lb(sw, (int)Mf, x);
-    if (Uout) Uout[f * Nf + i] = x;
+  if (a.Wout) {
+    for (int j = threadIdx.x; j < len; j += THREADS) {
+      const int c = j / K_TABLE;
+      const double S = __dadd_rn(Pr, __dadd_rn(s_R[c >> 5], __dadd_rn(sQ[c], sw[j])));
+      a.Wout[f * Mf + j0 + j] = (j0 + j == Mf - 1) ? 1.0 : fmin(__ddiv_rn(S, T), 1.0);
+    }
   }
-  if (Wout)
-    for (int64_t i = threadIdx.x; i < Mf; i += THREADS) Wout[f * Mf + i] = sw[i];
 }
 
 }  // namespace drs
@@ -202,18 +325,36 @@ __global__ void __launch_bounds__(THREADS, 1)
 using namespace drs;
 
 extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64_t Nf,
-                                   const uint64_t* keys, double* W, double* U, int64_t* out,
-                                   int32_t* status, void* stream) {
+                                   uint64_t* keys, int32_t advance, double* W, double* U,
+                                   int64_t* out, int32_t* status, void* stream) {
   if (B < 0 || Mf < 1 || Nf < 0 || !status) return DRS_ERR_ARG;
   if (B > 0 && (!w || !keys || (Nf > 0 && !out))) return DRS_ERR_ARG;
-  if (cdiv(Mf, TS_TABLE) > MAX_TABLE_TILES) return DRS_ERR_ARG;
+  if ((uintptr_t)w & 7) return DRS_ERR_ALIGN;
+  const int ntt = (int)cdiv(Mf, TS_TABLE);
+  const int ntu = (int)cdiv(Nf + 1, TS_UNIF);
+  const size_t smem = (size_t)(TS_TABLE + THREADS + ((Nf + 1 + 15) & ~(int64_t)15)) * 8;
+  if (ntt > MAX_TT || ntu > MAX_UT || smem > (size_t)(227 * 1024 - 1024)) return DRS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
   if (B == 0) return DRS_OK;
-  const int64_t smem = (cdiv(Mf, TS_TABLE) * TS_TABLE + Nf + 1) * 8;
-  if (smem > 227 * 1024 - 1024) return DRS_ERR_ARG;
-  cudaFuncSetAttribute(k_resample_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_resample_batched<<<(unsigned)B, THREADS, (size_t)smem, st>>>(w, Mf, Nf, keys, W, U, out, status);
-  const cudaError_t e = cudaGetLastError();
+  static size_t c_smem = 0;  // attribute raised once per size (only launches under graph capture)
+  if (c_smem < smem) {
+    cudaFuncSetAttribute(k_resample_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    c_smem = smem;
+  }
+  BatchedArgs a{w, B, Mf, Nf, keys, advance, W, U, out, status, ntt, ntu};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * ntt));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)ntt;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_resample_batched, a);
   return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }

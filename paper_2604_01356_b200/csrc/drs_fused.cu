@@ -194,9 +194,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   __shared__ __align__(8) uint64_t bar;
   __shared__ double s_g[WARPS];
   __shared__ double s_last[WARPS];
-  __shared__ double s_P, s_total;
+  __shared__ double s_C, s_P, s_total;
   __shared__ unsigned long long s_min;
   __shared__ uint32_t s_flag;
+  __shared__ uint64_t s_words[PhiloxSpacings::SMEM_WORDS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = blockIdx.x;
   const int64_t nt = gridDim.x;
@@ -220,20 +221,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   const int64_t e0 = t * TS_U + (int64_t)(warp * LANES + lane) * K_UNIF;
   double z[4];
   if (a.raw) {  // uniforms supplied by a host stream
-#pragma unroll
-    for (int i = 0; i < 4; ++i) z[i] = (e0 + i <= n) ? neglog(a.raw[e0 + i]) : 0.0;
-  } else {
-    const uint64_t d0 = offset + (uint64_t)e0;
-    const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
-    const U64x4 v0 = philox_block(a.k0, a.k1, b0);
-    U64x4 v1 = v0;
-    if (b1 != b0) v1 = philox_block(a.k0, a.k1, b1);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint64_t dd = d0 + (uint64_t)i;
-      const uint64_t raw = ((dd >> 2) == b0) ? pick(v0, (int)(dd & 3)) : pick(v1, (int)(dd & 3));
-      z[i] = (e0 + i <= n) ? neglog(u01(raw)) : 0.0;
-    }
+    const ArraySpacings src{a.raw};
+    src.tile4(t, n + 1, 0, nullptr, z);
+  } else {      // each Philox block generated once, shared through shared memory
+    const PhiloxSpacings src{a.k0, a.k1, offset, nullptr};
+    src.tile4(t, n + 1, offset, s_words, z);
   }
   unsigned long long mn = 0x7FF0000000000000ULL;
 #pragma unroll
@@ -255,8 +247,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   grid_barrier(bcount, bgen);
   if (a.offset_dev && t == 0 && threadIdx.x == 0) *a.offset_dev = offset + (uint64_t)(n + 1);
   if (warp == 0) {
-    // lanes stage 32 totals at a time; lane 0 folds them in tile order
-    double P = 0.0, total = 0.0;
+    // lanes stage 32 totals at a time and the tile chain is folded in tile
+    // order: D inside a group of GROUP_TILES tiles, C over the groups
+    double C = 0.0, D = 0.0, Ct = 0.0, Dt = 0.0;
     unsigned long long gmin = 0x7FF0000000000000ULL;
     for (int64_t base = 0; base < nt; base += 32) {
       const int64_t tt = base + lane;
@@ -268,34 +261,43 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
       double vk[32];
 #pragma unroll
       for (int k = 0; k < 32; ++k) vk[k] = __shfl_sync(FULL, v, k);
+      if (base > 0 && base % GROUP_TILES == 0) {  // group boundary (32 | GROUP_TILES)
+        C = __dadd_rn(C, D);
+        D = 0.0;
+      }
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        P = (base + k == t) ? total : P;
-        total = __dadd_rn(total, vk[k]);
+        Ct = (base + k == t) ? C : Ct;
+        Dt = (base + k == t) ? D : Dt;
+        D = __dadd_rn(D, vk[k]);
       }
     }
+    const double total = __dadd_rn(C, D);
     for (int o = 16; o > 0; o >>= 1) gmin = min(gmin, __shfl_xor_sync(FULL, gmin, o));
     if (lane == 0) {
-      s_P = P;
+      s_C = Ct;
+      s_P = Dt;
       s_total = total;
       s_min = gmin;
     }
   }
   __syncthreads();
-  const double P = s_P, total = s_total;
+  const double Cg = s_C, P = s_P, total = s_total;
   const double zmin = __longlong_as_double((long long)s_min);
   const bool need = !(zmin > __dmul_rn(1e-14, total));
 
   // 4. U in registers
   double u[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) u[i] = __ddiv_rn(__dadd_rn(P, __dadd_rn(R, __dadd_rn(Q, sc[i]))), total);
+  for (int i = 0; i < 4; ++i)
+    u[i] = __ddiv_rn(__dadd_rn(Cg, __dadd_rn(P, __dadd_rn(R, __dadd_rn(Q, sc[i])))), total);
 
   if (need) {  // grid-uniform: the reference's exactness check (randkit.py:95-100)
     double prev_lane = __shfl_up_sync(FULL, u[3], 1);
     if (lane == 31) s_last[warp] = u[3];
     __syncthreads();
-    if (lane == 0) prev_lane = (warp > 0) ? s_last[warp - 1] : ((t == 0) ? 0.0 : __ddiv_rn(P, total));
+    if (lane == 0)
+      prev_lane = (warp > 0) ? s_last[warp - 1] : ((t == 0) ? 0.0 : __ddiv_rn(__dadd_rn(Cg, P), total));
     bool site = false;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {

@@ -3,14 +3,18 @@
 //   K1 build_table     (cdf.py:59-89)      raw w -> W = S/T, W[M-1] == 1, + search index
 //   K2 sorted_uniforms (randkit.py:70-101) Philox draws -> -log -> Z -> U = Z/Z[n], + repair
 //
-// Both are reduce-then-scan over tiles of THREADS*K elements:
-//   pass 1: tile aggregate A_t (chained fold), then a
-//           decoupled look-back publishes the chained inclusive prefix
-//           incl[t] = incl[t-1] + A_t (left fold from the nearest published
-//           inclusive, so the value is the same whichever predecessor was found);
-//   pass 2: recompute the tile chain, S = P + (R + (Q + s)), apply the epilogue.
+// Both are reduce-then-scan over tiles of THREADS*K elements, with the
+// deterministic chained association of DESIGN.md section 4:
+//   pass 1       : tile totals A_t (in-tile chained fold) -- fully parallel;
+//   chain groups : one CTA folds the tile totals serially inside groups of
+//                  GROUP_TILES tiles (D_t) and the group totals serially (C_g);
+//                  no look-back, so no serial chain of inter-CTA round trips;
+//   pass 2       : S = C_g + (D_t + (R + (Q + s))) and the epilogue.
+// Every fold is a left fold from 0.0 and every group's last value is the next
+// group's base, so S is monotone and S[last] == T exactly.
 // The table pass reads w twice and writes W once (24 bytes per entry); the
-// uniform pass regenerates its draws in pass 2 and writes only U (8 bytes per u).
+// uniform pass generates each draw once, writes the in-tile sums in pass 1 and
+// turns them into U in pass 2 (24 bytes per u).
 #include "drs_common.cuh"
 
 namespace drs {
@@ -33,7 +37,7 @@ __host__ inline ScanWS carve(void* ws, size_t ws_bytes) {
   ScanWS s;
   s.hdr = (ScanHdr*)b;
   size_t o = kHdr;
-  s.flags = (uint32_t*)(b + o);
+  s.grp = (double*)(b + o);  // 4 bytes per tile hold the 8-byte group bases (GROUP_TILES >= 2)
   o += 4 * (size_t)C;
   o = (o + 15) & ~(size_t)15;
   s.agg = (double*)(b + o);
@@ -45,9 +49,10 @@ __host__ inline ScanWS carve(void* ws, size_t ws_bytes) {
 }
 
 __global__ void k_ws_init(ScanHdr* h) {
-  h->ticket = 0; h->done1 = 0; h->done2 = 0; h->epoch = 1;
+  h->done2 = 0;
   h->status = 0; h->nsites = 0; h->top = 0; h->bar_count = 0; h->bar_gen = 0;
   h->zmin_bits = 0x7FF0000000000000ULL;
+  h->total = 0.0;
 }
 
 // --------------------------------------------------------- tile chain ----
@@ -74,87 +79,104 @@ __device__ __forceinline__ double chain_fold(double tau, double* s_g, double& Q,
   return r;
 }
 
-// Decoupled look-back, executed by warp 0.  Returns the exclusive prefix P_t.
-// The warp inspects 32 predecessors at a time; a window holding only
-// aggregates is stashed in shared memory and the walk continues further back
-// (up to LB_MAXW windows), so the inclusive frontier is never a bottleneck.
-// The prefix is always the left fold incl[k] + agg[k+1] + ... + agg[t-1]
-// from the nearest published inclusive k, which equals the chained value
-// incl[t-1] bit for bit whichever k was found.
-constexpr int LB_MAXW = 16;
+// The tile chain: one CTA folds the nt tile totals.  Thread g folds group g
+// serially (D_t, exclusive) and leaves the group total; thread 0 then folds
+// the group totals serially (C_g, exclusive) and writes T = C_ng.  It also
+// finishes what needs every tile: for a table (mode 0) the status word (and
+// T for a shard scan); for sorted uniforms (mode 1) the minimum spacing
+// (pass 1 left each tile's minimum in incl[t]) and the reference's
+// exactness trigger zmin <= 1e-14 T (randkit.py:95).
+constexpr int CHAIN_THREADS = 512;
+constexpr int64_t CHAIN_CHUNK = 64 * GROUP_TILES;  // tiles staged in shared memory per round
+constexpr int CHAIN_MAX_GROUPS = 4096;              // nt <= 2^20 tiles
+constexpr size_t CHAIN_SMEM = (size_t)CHAIN_CHUNK * 8 + (size_t)CHAIN_MAX_GROUPS * 8;
 
-__device__ double lookback(const ScanWS& ws, int64_t t, uint32_t ep, double A, double* s_win) {
-  const int lane = threadIdx.x & 31;
-  if (t == 0) {
-    const double I = __dadd_rn(0.0, A);
-    if (lane == 0) {
-      st_relaxed_f64(&ws.incl[0], I);
-      st_release_u32(&ws.flags[0], (ep << 2) | 2u);
+__global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64_t nt, int mode,
+                                                               int32_t* status_out, double* total_out) {
+  extern __shared__ __align__(16) double csm[];
+  double* sa = csm;                // [CHAIN_CHUNK] tile totals -> exclusive in-group folds
+  double* sE = csm + CHAIN_CHUNK;  // [ng] group totals -> group bases
+  __shared__ unsigned long long s_min;
+  if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
+  const int64_t ng = cdiv(nt, GROUP_TILES);
+  unsigned long long mn = 0x7FF0000000000000ULL;
+  for (int64_t c0 = 0; c0 < nt; c0 += CHAIN_CHUNK) {
+    const int64_t c1 = (c0 + CHAIN_CHUNK < nt) ? c0 + CHAIN_CHUNK : nt;
+    // 1. stage the chunk's tile totals (coalesced, all loads in flight)
+    for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) {
+      sa[t - c0] = ws.agg[t];
+      if (mode == 1) mn = min(mn, (unsigned long long)__double_as_longlong(ws.incl[t]));
     }
-    return 0.0;
-  }
-  if (lane == 0) {
-    st_relaxed_f64(&ws.agg[t], A);
-    st_release_u32(&ws.flags[t], (ep << 2) | 1u);
-  }
-  int64_t base = t - 1;
-  int nw = 0;
-  double P = 0.0;
-  int spins = 0;
-  while (true) {
-    const int64_t tt = base - lane;
-    uint32_t st = 0;
-    if (tt >= 0) {
-      const uint32_t f = ld_acquire_u32(&ws.flags[tt]);
-      st = ((f >> 2) == ep) ? (f & 3u) : 0u;
-    }
-    const uint32_t incl_mask = __ballot_sync(FULL, st == 2u);
-    const uint32_t avail_mask = __ballot_sync(FULL, st != 0u);
-    if (incl_mask) {
-      const int j = __ffs(incl_mask) - 1;
-      const uint32_t need = (j == 0) ? 0u : ((1u << j) - 1u);
-      if ((avail_mask & need) == need) {
-        double val = 0.0;
-        if (lane == j) val = ld_relaxed_f64(&ws.incl[tt]);
-        else if (lane < j) val = ld_relaxed_f64(&ws.agg[tt]);
-        P = __shfl_sync(FULL, val, j);
-        for (int k = j - 1; k >= 0; --k) P = __dadd_rn(P, __shfl_sync(FULL, val, k));
-        break;
+    __syncthreads();
+    // 2. one thread per group: serial left fold from shared memory
+    const int64_t g0 = c0 / GROUP_TILES, g1 = cdiv(c1, GROUP_TILES);
+    for (int64_t g = g0 + threadIdx.x; g < g1; g += CHAIN_THREADS) {
+      const int64_t t0 = g * GROUP_TILES - c0;
+      const int64_t t1 = ((g + 1) * GROUP_TILES < c1 ? (g + 1) * GROUP_TILES : c1) - c0;
+      double D = 0.0;
+      int64_t t = t0;
+      for (; t + 8 <= t1; t += 8) {
+        double v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = sa[t + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          sa[t + k] = D;
+          D = __dadd_rn(D, v[k]);
+        }
       }
-    } else if (avail_mask == FULL && nw < LB_MAXW) {
-      s_win[nw * 32 + lane] = ld_relaxed_f64(&ws.agg[tt]);
-      __syncwarp();
-      ++nw;
-      base -= 32;
-      spins = 0;
-      continue;
+      for (; t < t1; ++t) {
+        const double v = sa[t];
+        sa[t] = D;
+        D = __dadd_rn(D, v);
+      }
+      sE[g] = D;
     }
-    if (++spins > 4) __nanosleep(32);
+    __syncthreads();
+    // 3. write the exclusive in-group folds back (coalesced)
+    for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) ws.incl[t] = sa[t - c0];
+    __syncthreads();
   }
-  for (int w = nw - 1; w >= 0; --w)
-    for (int k = 31; k >= 0; --k) P = __dadd_rn(P, s_win[w * 32 + k]);
-  const double I = __dadd_rn(P, A);
-  if (lane == 0) {
-    st_relaxed_f64(&ws.incl[t], I);
-    st_release_u32(&ws.flags[t], (ep << 2) | 2u);
-  }
-  return P;
-}
-
-// pass-1 epilogue common to all sources: completion count, epoch bump
-__device__ __forceinline__ void pass1_finish(const ScanWS& ws, uint32_t ep) {
+  if (mode == 1) atomicMin(&s_min, mn);
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&ws.hdr->done1, 1u) == gridDim.x - 1) {
-      uint32_t ne = (ep + 1) & 0x3FFFFFFFu;
-      if (ne == 0) ne = 1;
-      ws.hdr->epoch = ne;
-      ws.hdr->ticket = 0;
-      ws.hdr->done1 = 0;
-      __threadfence();
+    double C = 0.0;
+    for (int64_t g = 0; g < ng; ++g) {
+      const double e = sE[g];
+      sE[g] = C;
+      C = __dadd_rn(C, e);
+    }
+    const double T = C;
+    ws.hdr->total = T;
+    if (mode == 0) {
+      uint32_t st = ws.hdr->status;
+      if (T == 0.0) st |= DRS_ST_DEGENERATE;
+      if (!(T < dinf())) st |= DRS_ST_ACCUM_OVERFLOW;
+      if (status_out) *status_out = (int32_t)st;
+      if (total_out) *total_out = T;
+      ws.hdr->status = 0;
+    } else {
+      const double zmin = __longlong_as_double((long long)s_min);
+      ws.hdr->need = !(zmin > __dmul_rn(1e-14, T)) ? 1u : 0u;
     }
   }
+  __syncthreads();
+  for (int64_t g = threadIdx.x; g < ng; g += CHAIN_THREADS) ws.grp[g] = sE[g];
+}
+
+static void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total,
+                         cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chain_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
+    attr = true;
+  }
+  k_chain_groups<<<1, CHAIN_THREADS, CHAIN_SMEM, st>>>(s, nt, mode, status, total);
+}
+
+// exclusive chained prefix of tile t applied to an in-tile value y
+__device__ __forceinline__ double chain_apply(const ScanWS& ws, int64_t t, double y) {
+  return __dadd_rn(ws.grp[t / GROUP_TILES], __dadd_rn(ws.incl[t], y));
 }
 
 // ------------------------------------------------------------ K1 table ----
@@ -182,32 +204,30 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ double s_g[WARPS];
-  __shared__ int64_t s_tile;
-  __shared__ uint32_t s_ep;
-  __shared__ double s_win[LB_MAXW * 32];
-  if (threadIdx.x == 0) {
-    s_tile = (int64_t)atomicAdd(&ws.hdr->ticket, 1u);
-    s_ep = *(volatile uint32_t*)&ws.hdr->epoch;
-  }
-  __syncthreads();
-  const int64_t t = s_tile;
-  const uint32_t ep = s_ep;
-  stage_tile<K_TABLE>(w, n, t, sm, &bar);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* chunk = sm + (warp * LANES + lane) * K_TABLE;
-  double s = chunk[0];
-  bool bad = !(s >= 0.0 && s < dinf());
+  const int64_t t = blockIdx.x;
+  const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
+  const int c0 = threadIdx.x * K_TABLE;
+  const double* chunk = sm + c0;
+  // valid weight <=> 0 <= x < inf: screened from the high words (integer
+  // pipe); a set sign bit gets the exact check (-0.0 is a valid weight)
+  uint32_t any_sign = 0, max_mag = 0;
+  double s = 0.0;
 #pragma unroll
-  for (int i = 1; i < K_TABLE; ++i) {
+  for (int i = 0; i < K_TABLE; ++i) {
     const double x = chunk[i];
-    bad |= !(x >= 0.0 && x < dinf());
-    s = __dadd_rn(s, x);
+    const uint32_t hi = (uint32_t)__double2hiint(x);
+    any_sign |= hi;
+    max_mag = max(max_mag, hi & 0x7FFFFFFFu);
+    s = (i == 0) ? x : __dadd_rn(s, x);
   }
+  bool bad = max_mag >= 0x7FF00000u;
+  if (any_sign & 0x80000000u)
+    for (int i = 0; i < K_TABLE; ++i) bad |= !(chunk[i] >= 0.0);
   double Q, R;
   const double A = chain_fold(s, s_g, Q, R);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.hdr->status, (uint32_t)DRS_ST_INVALID_WEIGHT);
-  if (warp == 0) lookback(ws, t, ep, A, s_win);
-  pass1_finish(ws, ep);
+  if (threadIdx.x == 0) ws.agg[t] = A;
+  (void)len;
 }
 
 // RAW = false: W = min(S/T, 1) with W[n-1] = 1 and the index levels (dr_build_table)
@@ -231,15 +251,15 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
   for (int i = 1; i < K_TABLE; ++i) s = __dadd_rn(s, chunk[i]);
   double Q, R;
   chain_fold(s, s_g, Q, R);
-  const double P = (t == 0) ? 0.0 : ws.incl[t - 1];
-  const double T = ws.incl[nt - 1];
+  const double C = ws.grp[t / GROUP_TILES], D = ws.incl[t];
+  const double T = ws.hdr->total;
   const int64_t jb = t * TS + (int64_t)(warp * LANES + lane) * K_TABLE;
   double s2 = 0.0;
 #pragma unroll
   for (int i = 0; i < K_TABLE; ++i) {
     const double x = chunk[i];
     s2 = (i == 0) ? x : __dadd_rn(s2, x);
-    const double S = __dadd_rn(P, __dadd_rn(R, __dadd_rn(Q, s2)));
+    const double S = __dadd_rn(C, __dadd_rn(D, __dadd_rn(R, __dadd_rn(Q, s2))));
     const int64_t j = jb + i;
     if (RAW) {
       chunk[i] = S;
@@ -270,89 +290,59 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
       bulk_commit_wait();
     }
     if (len & 1) W[t * TS + len - 1] = sm[len - 1];
-    __threadfence();
-    if (atomicAdd(&ws.hdr->done2, 1u) == gridDim.x - 1) {
-      uint32_t st = *(volatile uint32_t*)&ws.hdr->status;
-      if (T == 0.0) st |= DRS_ST_DEGENERATE;
-      if (!(T < dinf())) st |= DRS_ST_ACCUM_OVERFLOW;
-      *status_out = (int32_t)st;
-      if (RAW) *total_out = T;
-      ws.hdr->status = 0;
-      ws.hdr->done2 = 0;
-      __threadfence();
-    }
   }
+  (void)status_out;
+  (void)total_out;
 }
 
 // ------------------------------------------------- K2 sorted uniforms ----
-// Spacing sources: element e (0 <= e <= n) of the n+1 spacings.
-struct PhiloxSpacings {
-  uint64_t k0, k1, offset;
-  const uint64_t* offset_dev;  // device-resident stream position (graph capture)
-  // the K_UNIF = 4 consecutive spacings starting at e0
-  __device__ __forceinline__ void chunk4(int64_t e0, int64_t count, double z[4]) const {
-    const uint64_t off = offset_dev ? *(volatile const uint64_t*)offset_dev : offset;
-    const uint64_t d0 = off + (uint64_t)e0;
-    const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
-    const U64x4 v0 = philox_block(k0, k1, b0);
-    U64x4 v1 = v0;
-    if (b1 != b0) v1 = philox_block(k0, k1, b1);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint64_t dd = d0 + (uint64_t)i;
-      const uint64_t raw = ((dd >> 2) == b0) ? pick(v0, (int)(dd & 3)) : pick(v1, (int)(dd & 3));
-      z[i] = (e0 + i < count) ? neglog(u01(raw)) : 0.0;
-    }
-  }
-};
-
-struct ArraySpacings {
-  const double* raw;
-  __device__ __forceinline__ void chunk4(int64_t e0, int64_t count, double z[4]) const {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) z[i] = (e0 + i < count) ? neglog(raw[e0 + i]) : 0.0;
-  }
-};
-
 __device__ __forceinline__ unsigned long long zmin_key(double z) {
   // positive doubles order like their bit patterns; NaN / <= 0 force the exact check
   if (!(z > 0.0)) return 0ull;
   return (unsigned long long)__double_as_longlong(z);
 }
 
+// pass 1: every spacing generated ONCE; the in-tile chained sums
+// R + (Q + sc) written to U (the tile prefix is applied in pass 2); the tile
+// total to agg[t]; the spacing minimum to the header.
 template <class Src>
-__global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, ScanWS ws) {
+__global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, ScanWS ws, double* __restrict__ Z) {
   __shared__ double s_g[WARPS];
-  __shared__ int64_t s_tile;
-  __shared__ uint32_t s_ep;
   __shared__ unsigned long long s_min;
-  __shared__ double s_win[LB_MAXW * 32];
-  if (threadIdx.x == 0) {
-    s_tile = (int64_t)atomicAdd(&ws.hdr->ticket, 1u);
-    s_ep = *(volatile uint32_t*)&ws.hdr->epoch;
-    s_min = 0x7FF0000000000000ULL;
-  }
-  __syncthreads();
-  const int64_t t = s_tile;
-  const uint32_t ep = s_ep;
+  __shared__ uint64_t s_words[Src::SMEM_WORDS];
+  if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
+  const int64_t t = blockIdx.x;
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t e0 = t * TS + (int64_t)(warp * LANES + lane) * K_UNIF;
+  const int64_t e0 = t * TS + (int64_t)threadIdx.x * K_UNIF;
   double z[4];
-  src.chunk4(e0, n + 1, z);
+  src.tile4(t, n + 1, src.position(), s_words, z);  // contains __syncthreads
   unsigned long long mn = 0x7FF0000000000000ULL;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
     if (e0 + i <= n) mn = min(mn, zmin_key(z[i]));
-  double s = z[0];
+  double sc[4];
+  sc[0] = z[0];
 #pragma unroll
-  for (int i = 1; i < 4; ++i) s = __dadd_rn(s, z[i]);
-  atomicMin(&s_min, mn);
+  for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+  if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
   double Q, R;
-  const double A = chain_fold(s, s_g, Q, R);  // contains __syncthreads
-  if (threadIdx.x == 0) atomicMin(&ws.hdr->zmin_bits, s_min);
-  if (warp == 0) lookback(ws, t, ep, A, s_win);
-  pass1_finish(ws, ep);
+  const double A = chain_fold(sc[3], s_g, Q, R);  // contains __syncthreads
+  if (threadIdx.x == 0) {
+    ws.agg[t] = A;
+    ws.incl[t] = __longlong_as_double((long long)s_min);  // folded by k_chain_groups
+  }
+  if (e0 + 3 < n && ((uintptr_t)Z & 31) == 0) {
+    double4 v;
+    v.x = __dadd_rn(R, __dadd_rn(Q, sc[0]));
+    v.y = __dadd_rn(R, __dadd_rn(Q, sc[1]));
+    v.z = __dadd_rn(R, __dadd_rn(Q, sc[2]));
+    v.w = __dadd_rn(R, __dadd_rn(Q, sc[3]));
+    *reinterpret_cast<double4*>(Z + e0) = v;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (e0 + i < n) Z[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
+  }
 }
 
 __device__ void repair_sites(double* U, int64_t n, const ScanWS& ws, uint32_t nsites, bool top) {
@@ -402,34 +392,32 @@ __device__ void repair_sites(double* U, int64_t n, const ScanWS& ws, uint32_t ns
   }
 }
 
-template <class Src>
-__global__ void __launch_bounds__(THREADS) k_unif_pass2(Src src, int64_t n, int64_t nt, ScanWS ws,
-                                                        double* __restrict__ U,
-                                                        int32_t* status_out) {
-  __shared__ double s_g[WARPS];
+// pass 2: U = Z / Z[n] in place (memory-bound: 16 bytes per u), collapse
+// sites recorded when the reference's exactness check fires (the repair and
+// the device stream advance follow in k_unif_finalize).
+__global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, ScanWS ws, double* __restrict__ U) {
   __shared__ double s_last[WARPS];
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
   const int64_t t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t e0 = t * TS + (int64_t)(warp * LANES + lane) * K_UNIF;
-  double z[4];
-  src.chunk4(e0, n + 1, z);
-  double sc[4];
-  sc[0] = z[0];
-#pragma unroll
-  for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
-  double Q, R;
-  chain_fold(sc[3], s_g, Q, R);
-  const double P = (t == 0) ? 0.0 : ws.incl[t - 1];
-  const double total = ws.incl[nt - 1];
-  const double zmin = __longlong_as_double((long long)*(volatile unsigned long long*)&ws.hdr->zmin_bits);
-  const bool need = !(zmin > __dmul_rn(1e-14, total));
+  const int64_t e0 = t * TS + (int64_t)threadIdx.x * K_UNIF;
+  const double total = ws.hdr->total;
+  const double C = ws.grp[t / GROUP_TILES], D = ws.incl[t];
+  const bool need = ws.hdr->need != 0u;
   double u[4];
+  if (e0 + 3 < n && ((uintptr_t)U & 31) == 0) {
+    const double4 v = *reinterpret_cast<const double4*>(U + e0);
+    u[0] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.x)), total);
+    u[1] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.y)), total);
+    u[2] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.z)), total);
+    u[3] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.w)), total);
+    *reinterpret_cast<double4*>(U + e0) = make_double4(u[0], u[1], u[2], u[3]);
+  } else {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double Z = __dadd_rn(P, __dadd_rn(R, __dadd_rn(Q, sc[i])));
-    u[i] = __ddiv_rn(Z, total);
-    if (e0 + i < n) U[e0 + i] = u[i];
+    for (int i = 0; i < 4; ++i) {
+      u[i] = (e0 + i < n) ? __ddiv_rn(__dadd_rn(C, __dadd_rn(D, U[e0 + i])), total) : 2.0;
+      if (e0 + i < n) U[e0 + i] = u[i];
+    }
   }
   if (need) {
     // previous U for each element: inside the chunk, from lane-1, from the
@@ -438,8 +426,10 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(Src src, int64_t n, int6
     if (lane == 31) s_last[warp] = u[3];
     __syncthreads();
     if (lane == 0) {
+      // the previous tile's last Z is its inclusive prefix, C + D of tile t
+      // (or, at a group boundary, C_g = C_{g-1} + E_{g-1}: the same value)
       if (warp > 0) prev_lane = s_last[warp - 1];
-      else prev_lane = (t == 0) ? 0.0 : __ddiv_rn(P, total);
+      else prev_lane = (t == 0) ? 0.0 : __ddiv_rn(__dadd_rn(C, D), total);
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -454,26 +444,22 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(Src src, int64_t n, int6
       }
     }
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&ws.hdr->done2, 1u) == gridDim.x - 1) {
-      __threadfence();
-      const uint32_t nsites = *(volatile uint32_t*)&ws.hdr->nsites;
-      const uint32_t top = *(volatile uint32_t*)&ws.hdr->top;
-      int32_t st = 0;
-      if (need && (nsites > 0 || top)) {
-        repair_sites(U, n, ws, nsites, top != 0);
-        st |= DRS_ST_REPAIRED;
-      }
-      *status_out = st;
-      ws.hdr->nsites = 0;
-      ws.hdr->top = 0;
-      ws.hdr->zmin_bits = 0x7FF0000000000000ULL;
-      ws.hdr->done2 = 0;
-      __threadfence();
-    }
+}
+
+// after pass 2: the repair when pass 2 found collapse sites, the status word,
+// the device stream advance, counters back to zero
+__global__ void k_unif_finalize(ScanWS ws, int64_t n, double* U, int32_t* status_out, uint64_t* offset_dev) {
+  const uint32_t nsites = ws.hdr->nsites;
+  const uint32_t top = ws.hdr->top;
+  int32_t st = 0;
+  if (ws.hdr->need && (nsites > 0 || top)) {
+    repair_sites(U, n, ws, nsites, top != 0);
+    st |= DRS_ST_REPAIRED;
   }
+  *status_out = st;
+  if (offset_dev) *offset_dev += (uint64_t)(n + 1);  // every pass-1 CTA has read it
+  ws.hdr->nsites = 0;
+  ws.hdr->top = 0;
 }
 
 // ------------------------------------------------------------- uniforms ----
@@ -535,12 +521,15 @@ ScanWS carve_ws(void* ws, size_t ws_bytes) { return carve(ws, ws_bytes); }
 
 template <class Src>
 static int sorted_impl(const Src& src, int64_t n, double* U, int32_t* status, void* ws,
-                       size_t ws_bytes, cudaStream_t st) {
+                       size_t ws_bytes, uint64_t* offset_dev, cudaStream_t st) {
   const int64_t nt = cdiv(n + 1, (int64_t)THREADS * K_UNIF);
   if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
   const ScanWS s = carve(ws, ws_bytes);
-  k_unif_pass1<Src><<<(unsigned)nt, THREADS, 0, st>>>(src, n, s);
-  k_unif_pass2<Src><<<(unsigned)nt, THREADS, 0, st>>>(src, n, nt, s, U, status);
+  k_unif_pass1<Src><<<(unsigned)nt, THREADS, 0, st>>>(src, n, s, U);
+  launch_chain(s, nt, 1, nullptr, nullptr, st);
+  k_unif_pass2<<<(unsigned)nt, THREADS, 0, st>>>(n, nt, s, U);
+  k_unif_finalize<<<1, 1, 0, st>>>(s, n, U, status, offset_dev);
   return launch_rc();
 }
 
@@ -548,16 +537,13 @@ int sorted_uniforms_launch(uint64_t k0, uint64_t k1, uint64_t offset, const uint
                            int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes,
                            cudaStream_t st) {
   PhiloxSpacings src{k0, k1, offset, offset_dev};
-  const int rc = sorted_impl(src, n, U, status, ws, ws_bytes, st);
-  if (rc || !offset_dev) return rc;
-  k_advance_offset<<<1, 1, 0, st>>>(const_cast<uint64_t*>(offset_dev), (uint64_t)(n + 1));
-  return launch_rc();
+  return sorted_impl(src, n, U, status, ws, ws_bytes, const_cast<uint64_t*>(offset_dev), st);
 }
 
 int sorted_uniforms_from_launch(const double* raw, int64_t n, double* U, int32_t* status, void* ws,
                                 size_t ws_bytes, cudaStream_t st) {
   ArraySpacings src{raw};
-  return sorted_impl(src, n, U, status, ws, ws_bytes, st);
+  return sorted_impl(src, n, U, status, ws, ws_bytes, nullptr, st);
 }
 
 }  // namespace drs
@@ -580,8 +566,18 @@ const char* dr_strerror(int code) {
   }
 }
 
-void dr_scan_geometry(int32_t g[5]) {
-  g[0] = LANES; g[1] = WARPS; g[2] = K_TABLE; g[3] = K_UNIF; g[4] = FANOUT;
+int dr_device_accessible(const void* p) {
+  cudaPointerAttributes a;
+  if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return 1;
+  return (a.type == cudaMemoryTypeHost && a.devicePointer == p) ? 1 : 0;
+}
+
+void dr_scan_geometry(int32_t g[6]) {
+  g[0] = LANES; g[1] = WARPS; g[2] = K_TABLE; g[3] = K_UNIF; g[4] = FANOUT; g[5] = GROUP_TILES;
 }
 
 size_t dr_workspace_bytes(int op, int64_t M, int64_t N, int64_t B) {
@@ -610,11 +606,13 @@ int dr_build_table(const double* w, int64_t M, double* W, double* idx, int32_t* 
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
   const int64_t nt = cdiv(M, (int64_t)THREADS * K_TABLE);
   if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
   set_attrs();
   const ScanWS s = carve(ws, ws_bytes);
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
   k_table_pass1<<<(unsigned)nt, THREADS, smem, st>>>(w, M, s);
+  launch_chain(s, nt, 0, status, nullptr, st);
   k_table_pass2<false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, nt, s, W, idx, d, status, nullptr);
   return launch_rc();
 }
@@ -625,12 +623,14 @@ int dr_shard_scan(const double* w_shard, int64_t Mg, double* S, double* Tg, int3
   if (((uintptr_t)w_shard | (uintptr_t)S) & 15) return DRS_ERR_ALIGN;
   const int64_t nt = cdiv(Mg, (int64_t)THREADS * K_TABLE);
   if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
   set_attrs();
   const ScanWS s = carve(ws, ws_bytes);
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
   const IndexDesc d = make_index_desc(Mg);
   k_table_pass1<<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, s);
+  launch_chain(s, nt, 0, status, Tg, st);
   k_table_pass2<true><<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, nt, s, S, nullptr, d, status, Tg);
   return launch_rc();
 }
@@ -654,7 +654,7 @@ int dr_sorted_uniforms_from(const double* raw, int64_t n, double* U, int32_t* st
                             size_t ws_bytes, void* stream) {
   if (n < 1 || !raw || !U || !status || !ws) return DRS_ERR_ARG;
   ArraySpacings src{raw};
-  return sorted_impl(src, n, U, status, ws, ws_bytes, (cudaStream_t)stream);
+  return sorted_impl(src, n, U, status, ws, ws_bytes, nullptr, (cudaStream_t)stream);
 }
 
 }  // extern "C"

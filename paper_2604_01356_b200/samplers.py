@@ -24,7 +24,15 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._tensors import empty_i64, is_device_tensor, read_status, status_word, to_device_f64
+from ._tensors import (
+    empty_i64,
+    finish_host,
+    host_result_i64,
+    is_device_tensor,
+    read_status,
+    status_word,
+    to_device_f64,
+)
 from .cdf import WeightTable
 from .randkit import DeviceRngStream, RngStream, sorted_uniforms_device
 
@@ -112,7 +120,7 @@ def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto"):
     if check:
         _check_sorted_open(ud)
     n = ud.numel()
-    out = empty_i64(n)
+    out = host_result_i64(n) if host else empty_i64(n)
     if n:
         L = _lib.lib()
         s = _lib.stream_handle()
@@ -123,7 +131,7 @@ def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto"):
             rc = L.dr_match_dac(W.data_ptr(), _ptr(table.device_index), table.size, ud.data_ptr(), n,
                                 out.data_ptr(), _lib.DAC_MODES[mode], s)
         _lib.check(rc, f"dr_match_{kind}")
-    return out.cpu().numpy() if host else out
+    return finish_host(out) if host else out
 
 
 def ccf_match(u, table: WeightTable, stats: OpStats | None = None, check: bool = True):
@@ -165,7 +173,9 @@ def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = N
     n = int(n)
     if n < 0:
         raise ValueError("negative dimensions are not allowed")
-    out = empty_i64(n) if out is None else out
+    to_host = out is None and not device
+    if out is None:
+        out = empty_i64(n) if device else host_result_i64(n)
     if n:
         W = table.device_cum
         if isinstance(stream, (RngStream, DeviceRngStream)):
@@ -175,7 +185,11 @@ def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = N
             _lib.check(rc, "dr_sample_binary_dev")
         else:
             us, _ = to_device_f64(stream.uniforms(n))
-            out = _lower_bounds(table, us)
+            res = _lower_bounds(table, us)
+            if res is not out:
+                out.copy_(res)
+    if to_host:
+        return finish_host(out)
     return out if device else out.cpu().numpy()
 
 
@@ -192,6 +206,20 @@ def _status_buf() -> torch.Tensor:
     return t
 
 
+_scratch_u: dict[int, torch.Tensor] = {}
+
+
+def _scratch_uniforms(n: int) -> torch.Tensor:
+    """Per-stream device scratch for U when the caller does not ask for it
+    (stream-ordered reuse is safe: every use is on the same stream)."""
+    s = _lib.stream_handle()
+    t = _scratch_u.get(s)
+    if t is None or t.numel() < n:
+        t = torch.empty(max(n, 1024), dtype=torch.float64, device=_lib.device())
+        _scratch_u[s] = t
+    return t
+
+
 def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None, U=None):
     _no_stats(stats, f"{kind}_sampler")
     n = int(n)
@@ -202,8 +230,10 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
         res = _match(kind, U, table, check=False, mode=mode)
         return res if device else res.cpu().numpy()
     L = _lib.lib()
-    out = empty_i64(n) if out is None else out
-    U = torch.empty(n, dtype=torch.float64, device=_lib.device()) if U is None else U
+    to_host = out is None and not device
+    if out is None:
+        out = empty_i64(n) if device else host_result_i64(n)
+    U = _scratch_uniforms(n) if U is None else U
     st = _status_buf()
     ws, wsb = _lib.workspace(L.dr_workspace_bytes(_lib.OP_SORTED, 0, n, 0))
     W = table.device_cum
@@ -214,6 +244,8 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
         rc = L.dr_sample_dac_from(W.data_ptr(), _ptr(table.device_index), table.size, raw.data_ptr(), n,
                                   U.data_ptr(), out.data_ptr(), st.data_ptr(), _lib.DAC_MODES[mode], ws, wsb, s)
         _lib.check(rc, "dr_sample_dac_from")
+        if to_host:
+            return finish_host(out)
         return out if device else out.cpu().numpy()
     k0, k1, off, offd = _stream_args(stream, n + 1)
     if kind == "ccf":
@@ -223,6 +255,8 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
         rc = L.dr_sample_dac(W.data_ptr(), _ptr(table.device_index), table.size, k0, k1, off, offd, n,
                              U.data_ptr(), out.data_ptr(), st.data_ptr(), _lib.DAC_MODES[mode], ws, wsb, s)
     _lib.check(rc, f"dr_sample_{kind}")
+    if to_host:
+        return finish_host(out)
     return out if device else out.cpu().numpy()
 
 

@@ -280,6 +280,66 @@ def test_batched_bit_exact_vs_oracle(drs, orc):
     np.testing.assert_array_equal(t.cum, W[5])
 
 
+@pytest.mark.parametrize("B,Mf,Nf", [(300, 16384, 256), (333, 16383, 257), (7, 12000, 3000), (5, 1, 4),
+                                     (200, 33, 1), (4, 8449, 1023), (3, 25000, 0)])
+def test_batched_shapes_vs_oracle(drs, orc, B, Mf, Nf):
+    """Tile edges, odd M_f (no TMA path), several table / uniform tiles, more
+    filters than resident CTAs, N_f = 0; bit-exact against the oracle."""
+    rng = np.random.default_rng(B * 7 + Mf)
+    w = np.exp(2.0 * rng.standard_normal((B, Mf)))
+    w[rng.random((B, Mf)) < 0.1] = 0.0
+    w[:, -1] += 1.0  # no degenerate filter
+    streams = [drs.RngStream(99, (b,)) for b in range(B)]
+    keys = np.array([[s.key[0], s.key[1], s.position] for s in streams], dtype=np.uint64)
+    res = drs.resample_batched(w, Nf, streams, return_uniforms=True, return_tables=True)
+    eo, Uo, Wo, st = orc.resample_batched(w, Nf, keys)
+    np.testing.assert_array_equal(res[2], Wo)
+    np.testing.assert_array_equal(res[1], Uo)
+    np.testing.assert_array_equal(res[0], eo)
+    assert all(s.position == (Nf + 1 if Nf else 0) for s in streams)
+
+
+def test_batched_device_streams_advance(drs, orc):
+    """BatchedStreams: positions advance on the device; two calls equal two
+    host-stream calls; CUDA-graph replay draws fresh uniforms."""
+    rng = np.random.default_rng(4)
+    B, Mf, Nf = 150, 4096, 100
+    w = np.exp(rng.standard_normal((B, Mf)))
+    host = [drs.RngStream(5, (b,)) for b in range(B)]
+    bs = drs.BatchedStreams([drs.RngStream(5, (b,)) for b in range(B)])
+    wd = dev(w)
+    for _ in range(2):
+        e = drs.resample_batched(w, Nf, host)
+        o = drs.resample_batched(wd, Nf, bs, check=False)
+        np.testing.assert_array_equal(o.cpu().numpy(), e)
+    assert (bs.positions() == 2 * (Nf + 1)).all()
+    out = torch.empty((B, Nf), dtype=torch.int64, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            r = drs.resample_batched(wd, Nf, bs, check=False)
+    torch.cuda.current_stream().wait_stream(side)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        e = drs.resample_batched(w, Nf, host)
+        np.testing.assert_array_equal(r.cpu().numpy(), e)
+    del out
+
+
+def test_batched_invalid_weights_raise(drs):
+    w = np.ones((10, 100))
+    w[3, 5] = -1.0
+    with pytest.raises(ValueError, match="invalid weight"):
+        drs.resample_batched(w, 8, [drs.RngStream(1, (b,)) for b in range(10)])
+    w = np.ones((10, 100))
+    w[7] = 0.0
+    with pytest.raises(ValueError, match="degenerate distribution"):
+        drs.resample_batched(w, 8, [drs.RngStream(1, (b,)) for b in range(10)])
+
+
 def test_sharded_single_gpu_emulation(drs, orc):
     """The shard steps for G shards run one after another on one GPU, with the
     all-gather replaced by stacking the totals; result == oracle sharded table."""
