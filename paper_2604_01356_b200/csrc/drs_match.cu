@@ -4,10 +4,9 @@
 //        one lane per u, 16-ary descent of the table's index: one 128-byte
 //        line (4 x 256-bit loads) per level, W itself only at the last level.
 //   K5 match_ccf                     (samplers.py:100-107, 162-188)
-//        W streamed once: each CTA takes a 4096-entry W tile by TMA bulk copy
-//        into shared memory, finds its U range [#u <= W[j0-1], #u <= W[j1])
-//        by warp-cooperative 32-ary searches of U, and merges that range
-//        against the tile (bisection for the first u of a run, cursor for the rest).
+//        W streamed once: one CTA per W tile (TMA bulk copy into shared
+//        memory), its u-run found by warp 32-ary searches of U, then a
+//        bisection per u (short runs) or merge path (long runs).
 //   K6 match_dac                     (samplers.py:110-146, 191-210)
 //        divide step = the U-range split by W tiles (merge mode) or by index
 //        blocks (search mode); AUTO picks merge when M <= tau*N.
@@ -61,7 +60,7 @@ __global__ void __launch_bounds__(256) k_sample_binary(const double* __restrict_
   if (i < N) out[i] = index_lower_bound(W, idx, d, u01(raw));
 }
 
-// -------------------------------------------------------- K5 merge tiles ----
+// -------------------------------------------------------- K5 merge stream ----
 // #(U[i] <= key) for sorted U, by a warp: 32-ary narrowing then one final probe.
 __device__ __forceinline__ int64_t warp_count_le(const double* __restrict__ U, int64_t N, double key) {
   const int lane = threadIdx.x & 31;
@@ -80,31 +79,51 @@ __device__ __forceinline__ int64_t warp_count_le(const double* __restrict__ U, i
   return lo + __popc(__ballot_sync(FULL, pred));
 }
 
-// first p in [0,n) with a[p] >= x, clamped to n-1 (the reference's bisection)
-__device__ __forceinline__ int smem_lower_bound(const double* a, int n, double x) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int m = (lo + hi) >> 1;
-    if (a[m] < x) lo = m + 1;
-    else hi = m;
+// #(a[i] <= key) for sorted a[0..n) in shared memory, by a warp
+__device__ __forceinline__ int warp_count_le_smem(const double* a, int n, double key) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = n;
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int p = lo + (lane + 1) * step - 1;
+    const int cnt = __popc(__ballot_sync(FULL, p < hi && a[p] <= key));
+    const int nhi = lo + (cnt + 1) * step - 1;
+    lo += cnt * step;
+    hi = nhi < hi ? nhi : hi;
   }
-  return lo;
+  return lo + __popc(__ballot_sync(FULL, lo + lane < hi && a[lo + lane] <= key));
 }
 
-__global__ void __launch_bounds__(256) k_merge_tiles(const double* __restrict__ W, int64_t M,
-                                                     const double* __restrict__ U, int64_t N,
-                                                     int64_t* __restrict__ out) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  double* sw = (double*)smraw;
-  int64_t* so = (int64_t*)(smraw + TW * sizeof(double));
+// The streaming merge (CCF, and DaC in merge mode).  One CTA per W tile of
+// `tw` entries (4096 at M >> N, smaller when the table is small so that every
+// SM holds several tiles): the tile arrives by one TMA bulk copy while two
+// warps find the tile's u-run [#(u <= W[j0-1]), #(u <= W[j0+len-1])) by
+// warp-cooperative 32-ary searches of U.  Several CTAs per SM keep HBM busy
+// (a probe of persistent TMA rings measured no better; profiles/r1_s3).
+// In the tile: a short u-run (M >> N) gets one shared-memory bisection per u;
+// a long one (M ~ N) is staged in shared memory and merged with the tile by
+// merge path -- every thread takes an equal diagonal segment, locates its
+// start by bisection and merges branch-free, taking W before u only when
+// W < u, so each u gets the first j with W[j] >= u.
+constexpr int MT_THREADS = 256;
+constexpr int MT_TW = 4096;   // max W entries per tile (32 KB)
+constexpr int MT_UC = 1024;   // u's staged per merge-path chunk (8 KB)
+
+__global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __restrict__ W, int64_t M,
+                                                            const double* __restrict__ U, int64_t N,
+                                                            int64_t* __restrict__ out, int tw) {
+  extern __shared__ __align__(128) double msm[];
+  double* sw = msm;            // [tw]
+  double* su = msm + tw;       // [MT_UC]
+  int64_t* so = (int64_t*)(su + MT_UC);  // [MT_UC] results, written out coalesced
   __shared__ __align__(8) uint64_t bar;
   __shared__ int64_t s_ib, s_ie;
   const int64_t t = blockIdx.x;
-  const int64_t j0 = t * TW;
-  const int len = (int)((M - j0) < TW ? (M - j0) : TW);
+  const int64_t j0 = t * tw;
+  const int len = (int)((M - j0) < tw ? (M - j0) : tw);
   const bool last = (j0 + len == M);
   const int len_even = len & ~1;
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
@@ -113,34 +132,55 @@ __global__ void __launch_bounds__(256) k_merge_tiles(const double* __restrict__ 
   if (threadIdx.x == 64 && (len & 1)) sw[len - 1] = W[j0 + len - 1];
   if (warp == 0) {
     const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, __ldg(W + j0 - 1));
-    if ((threadIdx.x & 31) == 0) s_ib = v;
+    if (lane == 0) s_ib = v;
   } else if (warp == 1) {
     const int64_t v = last ? N : warp_count_le(U, N, __ldg(W + j0 + len - 1));
-    if ((threadIdx.x & 31) == 0) s_ie = v;
+    if (lane == 0) s_ie = v;
   }
   __syncthreads();
   mbar_wait(&bar, 0);
   const int64_t ib = s_ib, ie = s_ie;
-  for (int64_t c0 = ib; c0 < ie; c0 += UCH) {
-    const int cl = (int)((ie - c0) < UCH ? (ie - c0) : UCH);
-    const int r = (cl + 255) / 256;
-    const int a = threadIdx.x * r;
-    const int b = (a + r < cl) ? (a + r) : cl;
-    if (a < b) {
-      double x = U[c0 + a];
-      int pos = smem_lower_bound(sw, len, x);
-      so[a] = j0 + pos;
-      for (int k = a + 1; k < b; ++k) {
-        x = U[c0 + k];
-        int steps = 0;
-        while (pos < len - 1 && sw[pos] < x && steps < 8) { ++pos; ++steps; }
-        if (pos < len - 1 && sw[pos] < x) pos = pos + 1 + smem_lower_bound(sw + pos + 1, len - pos - 1, x);
-        so[k] = j0 + pos;
+  if (ie - ib <= 2 * MT_THREADS) {
+    for (int64_t i = ib + threadIdx.x; i < ie; i += MT_THREADS) {
+      const double x = __ldg(U + i);
+      int lo = 0, hi = len - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (sw[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      out[i] = j0 + lo;
+    }
+    return;
+  }
+  for (int64_t c0 = ib; c0 < ie; c0 += MT_UC) {
+    const int c = (int)((ie - c0) < MT_UC ? (ie - c0) : MT_UC);
+    for (int i = threadIdx.x; i < c; i += MT_THREADS) su[i] = __ldg(U + c0 + i);
+    __syncthreads();
+    const int total = len + c;
+    const int per = (total + MT_THREADS - 1) / MT_THREADS;
+    const int d0 = min(total, (int)threadIdx.x * per), d1 = min(total, d0 + per);
+    int lo = max(0, d0 - c), hi = min(d0, len);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sw[mid] < su[d0 - mid - 1]) lo = mid + 1;
+      else hi = mid;
+    }
+    int ia = lo, ibb = d0 - lo;
+    for (int d = d0; d < d1; ++d) {
+      const double wa = (ia < len) ? sw[ia] : dinf();
+      const double xb = (ibb < c) ? su[ibb] : dinf();
+      if (ibb >= c || (ia < len && wa < xb)) {
+        ++ia;
+      } else {
+        so[ibb] = j0 + (ia < len ? ia : len - 1);  // clamp (u > 1 only without check)
+        ++ibb;
       }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < cl; k += 256) out[c0 + k] = so[k];
-    __syncthreads();
+    // coalesced (the destination may be pinned host memory written over the link)
+    for (int i = threadIdx.x; i < c; i += MT_THREADS) out[c0 + i] = so[i];
+    __syncthreads();  // su / so reuse
   }
 }
 
@@ -202,16 +242,22 @@ __global__ void k_lower_bound_range(const double* __restrict__ W, int64_t lo, in
   out[1] = probes;
 }
 
-static bool g_merge_attr = false;
 int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
-                        cudaStream_t st) {
-  const int smem = TW * 8 + UCH * 8;
-  if (!g_merge_attr) {
-    cudaFuncSetAttribute(k_merge_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    g_merge_attr = true;
+                 cudaStream_t st) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_merge_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((MT_TW + 2 * MT_UC) * sizeof(double)));
   }
-  const int64_t tiles = cdiv(M, TW);
-  k_merge_tiles<<<(unsigned)tiles, 256, smem, st>>>(W, M, U, N, out);
+  // tiles of up to 4096 entries; smaller for small tables so that every SM
+  // gets >= ~6 tiles to overlap
+  int tw = MT_TW;
+  while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
+  const size_t smem = (size_t)(tw + 2 * MT_UC) * sizeof(double);
+  k_merge_tiles<<<(unsigned)cdiv(M, tw), MT_THREADS, smem, st>>>(W, M, U, N, out, tw);
   return launch_rc();
 }
 
