@@ -207,7 +207,7 @@ def run_drs(args, rank, world, local_rank):
             return sampler(table, N, stream, device=True, out=out_buf, **kw)
 
         step = eager_step
-        fused = args.sampler == "dac" and args.mode != "merge" and M > 16 * N and (N + 1) <= 148 * 1024
+        fused = args.sampler == "dac" and args.mode != "merge" and M > 16 * N and (N + 1) <= 148 * 512
         launches_per_step = {"binary": 1, "ccf": 3}.get(args.sampler, 1 if fused else 3)
         if args.graph:
             # one sampler call captured once; the stream position lives on the

@@ -37,7 +37,7 @@ extern "C" {
 #define DRS_REF_LANES 32
 #define DRS_REF_WARPS 8
 #define DRS_REF_K_TABLE 33
-#define DRS_REF_K_UNIF 4
+#define DRS_REF_K_UNIF 2
 #define DRS_REF_FANOUT 16
 #define DRS_REF_GROUP 256 /* tiles per group of the tile chain */
 

@@ -142,15 +142,17 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
     unsigned long long mn = 0x7FF0000000000000ULL;
     for (int t = 0; t < a.ntu; ++t) {
       const int64_t e0 = t * TS_UNIF + (int64_t)threadIdx.x * K_UNIF;
-      double z[4] = {0.0, 0.0, 0.0, 0.0};
+      double z[K_UNIF];
+#pragma unroll
+      for (int i = 0; i < K_UNIF; ++i) z[i] = 0.0;
       if (e0 < ne) {
         const uint64_t d0 = off + (uint64_t)e0;
-        const uint64_t b0 = d0 >> 2, b1 = (d0 + 3) >> 2;
+        const uint64_t b0 = d0 >> 2, b1 = (d0 + K_UNIF - 1) >> 2;
         const U64x4 v0 = philox_block(k0, k1, b0);
         U64x4 v1 = v0;
         if (b1 != b0) v1 = philox_block(k0, k1, b1);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < K_UNIF; ++i) {
           const uint64_t dd = d0 + (uint64_t)i;
           const uint64_t raw = ((dd >> 2) == b0) ? pick(v0, (int)(dd & 3)) : pick(v1, (int)(dd & 3));
           if (e0 + i < ne) {
@@ -159,15 +161,15 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
           }
         }
       }
-      double sc[4];
+      double sc[K_UNIF];
       sc[0] = z[0];
 #pragma unroll
-      for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+      for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
       double Q, R;
-      const double A = tile_fold(sc[3], s_gu, Q, R);
+      const double A = tile_fold(sc[K_UNIF - 1], s_gu, Q, R);
       if (threadIdx.x == 0) s_Au[t] = A;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < K_UNIF; ++i)
         if (e0 + i < ne) su[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
       __syncthreads();  // s_gu reuse
     }

@@ -37,7 +37,30 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
 int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
                  int64_t* out, cudaStream_t st);
 
-constexpr int SIDX_CAP = 24576;  // doubles of index kept in shared memory (192 KB, 1 CTA per SM)
+#ifdef DRS_PHASE_TIMING
+// phase timestamps (profiling builds only): dbg[cta * 16 + phase] = %globaltimer
+__device__ unsigned long long g_phase[4096 * 16];
+#define STAMP(ph)                                                             \
+  do {                                                                        \
+    __syncthreads();                                                          \
+    if (threadIdx.x == 0) {                                                   \
+      unsigned long long tt_;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_));                \
+      g_phase[blockIdx.x * 16 + (ph)] = tt_;                                  \
+    }                                                                         \
+  } while (0)
+#else
+#define STAMP(ph) \
+  do {            \
+  } while (0)
+#endif
+
+constexpr int SIDX_CAP = 24576;
+constexpr int FUSED_MAX_TILES = 160;   // >= co-resident CTAs (148 SMs x 1); <= FLAG_CAP
+#ifndef DRS_L2_PREFETCH_MB
+#define DRS_L2_PREFETCH_MB 48
+#endif
+constexpr int64_t L2_PREFETCH_DOUBLES = (int64_t)DRS_L2_PREFETCH_MB << 17;  // MB of global index levels  // doubles of index kept in shared memory (192 KB, 1 CTA per SM)
 constexpr int64_t TS_U = (int64_t)THREADS * K_UNIF;
 
 struct SmemLevels {
@@ -96,39 +119,53 @@ __device__ __forceinline__ int64_t search_sm(const double* __restrict__ W, const
   return j0 + c;
 }
 
-// four independent searches in lock-step: the level loop is outside, so the
-// four lines of a level are in flight together
-__device__ __forceinline__ void search4_sm(const double* __restrict__ W, const double* __restrict__ idx,
-                                           const double* sidx, const IndexDesc& d, const SmemLevels& sl,
-                                           const double x[4], int64_t r[4]) {
-  int64_t b[4] = {0, 0, 0, 0};
+// K_UNIF independent searches in lock-step: the level loop is outside, so the
+// lines of a level are in flight together
+__device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const double* __restrict__ idx,
+                                            const double* sidx, const IndexDesc& d, const SmemLevels& sl,
+                                            const double x[K_UNIF], int64_t r[K_UNIF]) {
+  int64_t b[K_UNIF];
+#pragma unroll
+  for (int q = 0; q < K_UNIF; ++q) b[q] = 0;
   for (int k = d.levels; k >= 1; --k) {
-    int c[4];
+    int c[K_UNIF];
     if (k >= sl.k_smem) {
       const double* base = sidx + (d.off[k] - sl.base);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = count_lt16_smem(base + FANOUT * b[q], x[q]);
+      for (int q = 0; q < K_UNIF; ++q) c[q] = count_lt16_smem(base + FANOUT * b[q], x[q]);
     } else {
       const double* base = idx + d.off[k];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) c[q] = count_lt16(base + FANOUT * b[q], x[q]);
+      for (int q = 0; q < K_UNIF; ++q) c[q] = count_lt16(base + FANOUT * b[q], x[q]);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < K_UNIF; ++q) {
       const int64_t valid = d.n[k] - FANOUT * b[q];
       if (c[q] >= valid) c[q] = (int)valid - 1;
       b[q] = FANOUT * b[q] + c[q];
     }
   }
+  // W level: the lines are loaded together (branch-free addresses; the rare
+  // short tail line is re-read scalar), so the DRAM round trips overlap
+  double v[K_UNIF][16];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < K_UNIF; ++q) {
+    const int64_t j0 = FANOUT * b[q];
+    const double* p = (d.n[0] - j0 >= FANOUT) ? W + j0 : W;
+    ldg256(p + 0, v[q][0], v[q][1], v[q][2], v[q][3]);
+    ldg256(p + 4, v[q][4], v[q][5], v[q][6], v[q][7]);
+    ldg256(p + 8, v[q][8], v[q][9], v[q][10], v[q][11]);
+    ldg256(p + 12, v[q][12], v[q][13], v[q][14], v[q][15]);
+  }
+#pragma unroll
+  for (int q = 0; q < K_UNIF; ++q) {
     const int64_t j0 = FANOUT * b[q];
     const int64_t valid = d.n[0] - j0;
-    int c;
+    int c = 0;
     if (valid >= FANOUT) {
-      c = count_lt16(W + j0, x[q]);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c += (v[q][i] < x[q]) ? 1 : 0;
     } else {
-      c = 0;
       for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
     }
     if (c >= valid) c = (int)valid - 1;
@@ -205,102 +242,160 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   uint32_t* bcount = &a.ws.hdr->bar_count;
   uint32_t* bgen = &a.ws.hdr->bar_gen;
 
-  // 1. prefetch the top index levels (TMA bulk copy, overlaps step 2)
+  // 1. stage the top index levels in shared memory (TMA bulk copy) and
+  // prefetch the next global levels into L2 (one slice per CTA): both overlap
+  // steps 2-4, so the search finds them on chip instead of in HBM
   const uint32_t sbytes = (uint32_t)(a.sl.count * 8);
   if (threadIdx.x == 0) {
     s_min = 0x7FF0000000000000ULL;
     s_flag = 0;
+  }
+  // issued by the last warp: thread 0's release of the tile total below must
+  // not queue behind these bulk transfers
+  if (threadIdx.x == THREADS - 32) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, sbytes);
     if (sbytes) bulk_g2s(sidx, a.idx + a.sl.base, sbytes, &bar);
+    const int64_t plo = a.sl.base > L2_PREFETCH_DOUBLES ? a.sl.base - L2_PREFETCH_DOUBLES : 0;
+    const int64_t per = cdiv(cdiv(a.sl.base - plo, (int64_t)gridDim.x), 2) * 2;  // 16-byte multiples
+    const int64_t p0 = plo + t * per, p1 = min(a.sl.base, p0 + per) & ~(int64_t)1;
+    for (int64_t p = p0 & ~(int64_t)1; p < p1; p += 8192)  // 64 KB pieces
+      prefetch_l2(a.idx + p, (uint32_t)(min((int64_t)8192, p1 - p) * 8));
   }
+  const unsigned long long gen = *(volatile unsigned long long*)&a.ws.hdr->fgen;
   const uint64_t offset = a.offset_dev ? *(volatile uint64_t*)a.offset_dev : a.offset;
   __syncthreads();
+  STAMP(0);
 
   // 2. draws, spacings, tile chain
   const int64_t e0 = t * TS_U + (int64_t)(warp * LANES + lane) * K_UNIF;
-  double z[4];
+  double z[K_UNIF];
   if (a.raw) {  // uniforms supplied by a host stream
     const ArraySpacings src{a.raw};
-    src.tile4(t, n + 1, 0, nullptr, z);
+    src.tile(t, n + 1, 0, nullptr, z);
   } else {      // each Philox block generated once, shared through shared memory
     const PhiloxSpacings src{a.k0, a.k1, offset, nullptr};
-    src.tile4(t, n + 1, offset, s_words, z);
+    src.tile(t, n + 1, offset, s_words, z);
   }
+  STAMP(1);
   unsigned long long mn = 0x7FF0000000000000ULL;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < K_UNIF; ++i)
     if (e0 + i <= n) mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
-  double sc[4];
+  double sc[K_UNIF];
   sc[0] = z[0];
 #pragma unroll
-  for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+  for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
   atomicMin(&s_min, mn);
   double Q, R;
-  const double A = chain_fold_f(sc[3], s_g, Q, R);
+  const double A = chain_fold_f(sc[K_UNIF - 1], s_g, Q, R);
+  STAMP(2);
+  STAMP(3);
   if (threadIdx.x == 0) {
     st_relaxed_f64(&a.ws.agg[t], A);
     st_relaxed_f64(&a.ws.incl[t], __longlong_as_double((long long)s_min));
+    st_release_u64(&a.ws.tflag[t], gen + 1);  // tile t published for this call
   }
 
-  // 3. one grid barrier, then the chained fold of the tile totals before t
-  grid_barrier(bcount, bgen);
-  if (a.offset_dev && t == 0 && threadIdx.x == 0) *a.offset_dev = offset + (uint64_t)(n + 1);
-  if (warp == 0) {
-    // lanes stage 32 totals at a time and the tile chain is folded in tile
-    // order: D inside a group of GROUP_TILES tiles, C over the groups
-    double C = 0.0, D = 0.0, Ct = 0.0, Dt = 0.0;
+  // 3. the tile chain, folded once: CTA 0 waits for every tile's flag (at
+  // generation gen + 1), folds the totals in tile order (D inside groups of
+  // GROUP_TILES tiles, C over the groups), writes each tile's (C, D), the
+  // total and the spacing minimum, then releases hdr->fgen = gen + 1; every
+  // other CTA polls that single word (one poller per CTA, no all-to-all).
+  if (t == 0 && warp == 0) {
+    double va[FUSED_MAX_TILES / 32], vm[FUSED_MAX_TILES / 32];
+    double vc[FUSED_MAX_TILES / 32], vd[FUSED_MAX_TILES / 32];
+    while (true) {  // poll all flags together (independent loads)
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
+        const int64_t tt = q * 32 + lane;
+        if (tt < nt) ok &= (ld_acquire_u64(&a.ws.tflag[tt]) == gen + 1);
+      }
+      if (__all_sync(FULL, ok)) break;
+      __nanosleep(20);
+    }
+#pragma unroll
+    for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
+      const int64_t tt = q * 32 + lane;
+      va[q] = (tt < nt) ? ld_relaxed_f64(&a.ws.agg[tt]) : 0.0;
+      vm[q] = (tt < nt) ? ld_relaxed_f64(&a.ws.incl[tt]) : __longlong_as_double(0x7FF0000000000000LL);
+      vc[q] = 0.0;
+      vd[q] = 0.0;
+    }
+    double C = 0.0, D = 0.0;
     unsigned long long gmin = 0x7FF0000000000000ULL;
-    for (int64_t base = 0; base < nt; base += 32) {
-      const int64_t tt = base + lane;
-      const double v = (tt < nt) ? ld_relaxed_f64(&a.ws.agg[tt]) : 0.0;
-      const double m = (tt < nt) ? ld_relaxed_f64(&a.ws.incl[tt]) : __longlong_as_double(0x7FF0000000000000LL);
-      gmin = min(gmin, (unsigned long long)__double_as_longlong(m));
+#pragma unroll
+    for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
+      const int64_t base = q * 32;
+      if (base >= nt) break;
+      gmin = min(gmin, (unsigned long long)__double_as_longlong(vm[q]));
       // fully unrolled: the 32 shuffles issue back to back and only the adds
       // chain; tiles past nt contribute +0.0, which leaves the fold unchanged
       double vk[32];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) vk[k] = __shfl_sync(FULL, v, k);
+      for (int k = 0; k < 32; ++k) vk[k] = __shfl_sync(FULL, va[q], k);
       if (base > 0 && base % GROUP_TILES == 0) {  // group boundary (32 | GROUP_TILES)
         C = __dadd_rn(C, D);
         D = 0.0;
       }
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        Ct = (base + k == t) ? C : Ct;
-        Dt = (base + k == t) ? D : Dt;
+        vc[q] = (lane == k) ? C : vc[q];
+        vd[q] = (lane == k) ? D : vd[q];
         D = __dadd_rn(D, vk[k]);
       }
     }
     const double total = __dadd_rn(C, D);
     for (int o = 16; o > 0; o >>= 1) gmin = min(gmin, __shfl_xor_sync(FULL, gmin, o));
+#pragma unroll
+    for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
+      const int64_t tt = q * 32 + lane;
+      if (tt < nt) {
+        st_relaxed_f64(&a.ws.agg[tt], vd[q]);
+        st_relaxed_f64(&a.ws.incl[tt], vc[q]);
+      }
+    }
     if (lane == 0) {
-      s_C = Ct;
-      s_P = Dt;
+      s_C = vc[0];
+      s_P = vd[0];
       s_total = total;
       s_min = gmin;
+      a.ws.hdr->total = total;
+      a.ws.hdr->zmin_bits = gmin;
+      // every CTA has read the stream position and the generation
+      if (a.offset_dev) *a.offset_dev = offset + (uint64_t)(n + 1);
     }
+    __syncwarp();
+    if (lane == 0) st_release_u64(&a.ws.hdr->fgen, gen + 1);
+  } else if (t != 0 && threadIdx.x == 0) {
+    while (ld_acquire_u64(&a.ws.hdr->fgen) != gen + 1) __nanosleep(64);
+    s_C = ld_relaxed_f64(&a.ws.incl[t]);
+    s_P = ld_relaxed_f64(&a.ws.agg[t]);
+    s_total = ld_relaxed_f64(&a.ws.hdr->total);
+    s_min = *(volatile unsigned long long*)&a.ws.hdr->zmin_bits;
   }
   __syncthreads();
   const double Cg = s_C, P = s_P, total = s_total;
   const double zmin = __longlong_as_double((long long)s_min);
   const bool need = !(zmin > __dmul_rn(1e-14, total));
+  STAMP(4);
 
   // 4. U in registers
-  double u[4];
+  double u[K_UNIF];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < K_UNIF; ++i)
     u[i] = __ddiv_rn(__dadd_rn(Cg, __dadd_rn(P, __dadd_rn(R, __dadd_rn(Q, sc[i])))), total);
 
   if (need) {  // grid-uniform: the reference's exactness check (randkit.py:95-100)
-    double prev_lane = __shfl_up_sync(FULL, u[3], 1);
-    if (lane == 31) s_last[warp] = u[3];
+    double prev_lane = __shfl_up_sync(FULL, u[K_UNIF - 1], 1);
+    if (lane == 31) s_last[warp] = u[K_UNIF - 1];
     __syncthreads();
     if (lane == 0)
       prev_lane = (warp > 0) ? s_last[warp - 1] : ((t == 0) ? 0.0 : __ddiv_rn(__dadd_rn(Cg, P), total));
     bool site = false;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < K_UNIF; ++i) {
       const int64_t e = e0 + i;
       if (e < n) {
         const double pv = (i == 0) ? prev_lane : u[i - 1];
@@ -366,25 +461,29 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
       }
       grid_barrier(bcount, bgen);
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < K_UNIF; ++i)
         if (e0 + i < n) u[i] = ld_relaxed_f64(a.U + e0 + i);
     }
   }
 
-  // 5. search: 4 sorted u's per thread, top index levels in shared memory
+  // 5. search: K_UNIF sorted u's per thread, top index levels in shared memory
+  STAMP(5);
   mbar_wait(&bar, 0);
-  int64_t r[4];
-  search4_sm(a.W, a.idx, sidx, a.d, a.sl, u, r);
+  STAMP(6);
+  int64_t r[K_UNIF];
+  search_k_sm(a.W, a.idx, sidx, a.d, a.sl, u, r);
+  STAMP(7);
 
   // 6. write back
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < K_UNIF; ++i) {
     if (e0 + i < n) {
       a.out[e0 + i] = r[i];
       if (a.U && !need) a.U[e0 + i] = u[i];
     }
   }
   __syncthreads();
+  STAMP(8);
   if (t == 0 && threadIdx.x == 0) {
     // every CTA read the offset and the shared words before the last barrier
     *a.status = s_flag ? DRS_ST_REPAIRED : 0;
@@ -466,7 +565,7 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
   const int64_t nt = cdiv(N + 1, TS_U);
   const bool merge = (mode == DRS_DAC_MERGE) || (mode == DRS_DAC_AUTO && M <= 16 * N);
-  if (!merge && nt <= coop_capacity() && nt <= ws_capacity_tiles(ws_bytes)) {
+  if (!merge && nt <= coop_capacity() && nt <= FUSED_MAX_TILES && nt <= ws_capacity_tiles(ws_bytes)) {
     FusedArgs a;
     a.W = W; a.idx = idx; a.d = d; a.sl = plan_smem_levels(d);
     a.k0 = k0; a.k1 = k1; a.offset = offset; a.offset_dev = offset_dev; a.raw = raw;
@@ -485,6 +584,12 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
 }  // namespace drs
 
 extern "C" {
+
+#ifdef DRS_PHASE_TIMING
+int dr_debug_phase_times(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int dr_sample_dac_from(const double* W, const double* idx, int64_t M, const double* raw, int64_t N,
                        double* U, int64_t* out, int32_t* status, int32_t mode, void* ws,

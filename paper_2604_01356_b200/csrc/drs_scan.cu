@@ -22,7 +22,7 @@ namespace drs {
 // ------------------------------------------------------ workspace layout ----
 static constexpr size_t kHdr = 64;
 
-__host__ inline size_t ws_fixed_bytes() { return kHdr + 8 * (size_t)SITE_CAP + 64; }
+__host__ inline size_t ws_fixed_bytes() { return kHdr + 8 * (size_t)SITE_CAP + 8 * (size_t)FLAG_CAP + 64; }
 
 // The layout depends only on ws_bytes, so flag slots never alias value slots
 // across calls with different tile counts.
@@ -45,6 +45,8 @@ __host__ inline ScanWS carve(void* ws, size_t ws_bytes) {
   s.incl = (double*)(b + o);
   o += 8 * (size_t)C;
   s.sites = (long long*)(b + o);
+  o += 8 * (size_t)SITE_CAP;
+  s.tflag = (unsigned long long*)(b + o);
   return s;
 }
 
@@ -314,34 +316,32 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   const int64_t t = blockIdx.x;
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
   const int64_t e0 = t * TS + (int64_t)threadIdx.x * K_UNIF;
-  double z[4];
-  src.tile4(t, n + 1, src.position(), s_words, z);  // contains __syncthreads
+  double z[K_UNIF];
+  src.tile(t, n + 1, src.position(), s_words, z);  // contains __syncthreads
   unsigned long long mn = 0x7FF0000000000000ULL;
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < K_UNIF; ++i)
     if (e0 + i <= n) mn = min(mn, zmin_key(z[i]));
-  double sc[4];
+  double sc[K_UNIF];
   sc[0] = z[0];
 #pragma unroll
-  for (int i = 1; i < 4; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+  for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
   if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
   double Q, R;
-  const double A = chain_fold(sc[3], s_g, Q, R);  // contains __syncthreads
+  const double A = chain_fold(sc[K_UNIF - 1], s_g, Q, R);  // contains __syncthreads
   if (threadIdx.x == 0) {
     ws.agg[t] = A;
     ws.incl[t] = __longlong_as_double((long long)s_min);  // folded by k_chain_groups
   }
-  if (e0 + 3 < n && ((uintptr_t)Z & 31) == 0) {
-    double4 v;
-    v.x = __dadd_rn(R, __dadd_rn(Q, sc[0]));
-    v.y = __dadd_rn(R, __dadd_rn(Q, sc[1]));
-    v.z = __dadd_rn(R, __dadd_rn(Q, sc[2]));
-    v.w = __dadd_rn(R, __dadd_rn(Q, sc[3]));
-    *reinterpret_cast<double4*>(Z + e0) = v;
+  double v[K_UNIF];
+#pragma unroll
+  for (int i = 0; i < K_UNIF; ++i) v[i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
+  if (e0 + K_UNIF <= n && vec_ok(Z + e0)) {
+    store_k(Z + e0, v);
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (e0 + i < n) Z[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
+    for (int i = 0; i < K_UNIF; ++i)
+      if (e0 + i < n) Z[e0 + i] = v[i];
   }
 }
 
@@ -404,26 +404,25 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, S
   const double total = ws.hdr->total;
   const double C = ws.grp[t / GROUP_TILES], D = ws.incl[t];
   const bool need = ws.hdr->need != 0u;
-  double u[4];
-  if (e0 + 3 < n && ((uintptr_t)U & 31) == 0) {
-    const double4 v = *reinterpret_cast<const double4*>(U + e0);
-    u[0] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.x)), total);
-    u[1] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.y)), total);
-    u[2] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.z)), total);
-    u[3] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v.w)), total);
-    *reinterpret_cast<double4*>(U + e0) = make_double4(u[0], u[1], u[2], u[3]);
+  double u[K_UNIF];
+  if (e0 + K_UNIF <= n && vec_ok(U + e0)) {
+    double v[K_UNIF];
+    load_k(U + e0, v);
+#pragma unroll
+    for (int i = 0; i < K_UNIF; ++i) u[i] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, v[i])), total);
+    store_k(U + e0, u);
   } else {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < K_UNIF; ++i) {
       u[i] = (e0 + i < n) ? __ddiv_rn(__dadd_rn(C, __dadd_rn(D, U[e0 + i])), total) : 2.0;
       if (e0 + i < n) U[e0 + i] = u[i];
     }
   }
   if (need) {
     // previous U for each element: inside the chunk, from lane-1, from the
-    // previous warp, or from the previous tile's last Z (= incl[t-1])
-    double prev_lane = __shfl_up_sync(FULL, u[3], 1);
-    if (lane == 31) s_last[warp] = u[3];
+    // previous warp, or from the previous tile's last Z
+    double prev_lane = __shfl_up_sync(FULL, u[K_UNIF - 1], 1);
+    if (lane == 31) s_last[warp] = u[K_UNIF - 1];
     __syncthreads();
     if (lane == 0) {
       // the previous tile's last Z is its inclusive prefix, C + D of tile t
@@ -432,7 +431,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, S
       else prev_lane = (t == 0) ? 0.0 : __ddiv_rn(__dadd_rn(C, D), total);
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < K_UNIF; ++i) {
       const int64_t e = e0 + i;
       if (e < n) {
         const double pv = (i == 0) ? prev_lane : u[i - 1];

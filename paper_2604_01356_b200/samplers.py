@@ -271,7 +271,7 @@ def dac_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None
     """Sorted uniforms + divide-and-conquer (samplers.py:262-266).
 
     With a Philox stream this is one library call (``dr_sample_dac``): for
-    N+1 <= 1024 x (co-resident CTAs) a single cooperative kernel generates,
+    N+1 <= 512 x (co-resident CTAs) a single cooperative kernel generates,
     scans and normalises the uniforms in registers and searches them.
     ``out`` / ``uniforms_out`` take preallocated CUDA buffers.
     """
