@@ -69,6 +69,9 @@ const char *dr_strerror(int code);
  * or pinned host memory under unified addressing, which the search kernels
  * then write directly); 0 otherwise. */
 int dr_device_accessible(const void *p);
+/* cudaStreamSynchronize(stream): the host waits for a result written to
+ * pinned host memory (0 or DRS_ERR_LAUNCH) */
+int dr_stream_synchronize(void *stream);
 /* writes LANES, WARPS, K_TABLE, K_UNIF, FANOUT, GROUP into g[0..5] */
 void dr_scan_geometry(int32_t g[6]);
 

@@ -46,6 +46,7 @@ _PROTOS = {
     "dr_version": (ctypes.c_char_p, []),
     "dr_strerror": (ctypes.c_char_p, [_int]),
     "dr_device_accessible": (_int, [_c_void_p]),
+    "dr_stream_synchronize": (_int, [_c_void_p]),
     "dr_scan_geometry": (None, [_c_void_p]),
     "dr_workspace_bytes": (_size, [_int, _i64, _i64, _i64]),
     "dr_workspace_init": (_int, [_c_void_p, _size, _c_void_p]),
@@ -99,11 +100,17 @@ def load_library(path: Path | str | None = None):
         return lib
 
 
+_cuda_ok = False
+
+
 def lib():
-    """The bound library, after checking that a CUDA device is present."""
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2604_01356_b200 needs a CUDA device (sm_100a); none is visible")
-    return load_library()
+    """The bound library, after checking (once) that a CUDA device is present."""
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2604_01356_b200 needs a CUDA device (sm_100a); none is visible")
+        _cuda_ok = True
+    return _lib if _lib is not None else load_library()
 
 
 def check(rc: int, what: str) -> None:
@@ -124,7 +131,13 @@ def device_accessible(ptr: int) -> bool:
     return ok
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle() -> int:
+    """cudaStream_t of torch's current stream on the current device."""
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 
@@ -150,14 +163,27 @@ _ws: dict[tuple[int, int], _Workspace] = {}
 _ws_lock = threading.Lock()
 
 
-def workspace(nbytes: int) -> tuple[int, int]:
-    """(pointer, size) of the look-back workspace of the current (device, stream).
+_ws_bytes: dict[tuple[int, int], int] = {}
+
+
+def workspace_bytes(op: int, n: int) -> int:
+    """dr_workspace_bytes(op, n, n, 0), memoised (a pure function of its arguments)."""
+    v = _ws_bytes.get((op, n))
+    if v is None:
+        v = int(lib().dr_workspace_bytes(op, n, n, 0))
+        _ws_bytes[(op, n)] = v
+    return v
+
+
+def workspace(nbytes: int, st: int | None = None) -> tuple[int, int]:
+    """(pointer, size) of the scan workspace of the current (device, stream).
 
     Grown on demand; a new allocation is initialised with dr_workspace_init
     on the stream it will be used on.
     """
     dev = torch.cuda.current_device()
-    st = stream_handle()
+    if st is None:
+        st = stream_handle()
     with _ws_lock:
         w = _ws.setdefault((dev, st), _Workspace())
         if w.nbytes < nbytes:

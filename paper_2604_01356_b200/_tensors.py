@@ -75,7 +75,9 @@ def host_result_i64(n: int) -> torch.Tensor:
     return t
 
 
-def finish_host(t: torch.Tensor) -> np.ndarray:
+def finish_host(t: torch.Tensor, stream: int | None = None) -> np.ndarray:
     """Wait for the stream that wrote ``t`` (pinned host memory) and hand it out as numpy."""
-    torch.cuda.current_stream().synchronize()
+    if stream is None:
+        stream = _lib.stream_handle()
+    _lib.check(_lib.lib().dr_stream_synchronize(stream), "dr_stream_synchronize")
     return t.numpy()

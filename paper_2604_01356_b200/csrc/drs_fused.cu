@@ -474,12 +474,22 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   search_k_sm(a.W, a.idx, sidx, a.d, a.sl, u, r);
   STAMP(7);
 
-  // 6. write back
+  // 6. write back: one 16-byte store per lane when aligned, so a warp's
+  // stores cover whole lines (the destination may be pinned host memory)
+  if (K_UNIF == 2 && e0 + 2 <= n && (((uintptr_t)(a.out + e0)) & 15) == 0) {
+    *reinterpret_cast<longlong2*>(a.out + e0) = make_longlong2((long long)r[0], (long long)r[K_UNIF - 1]);
+  } else {
 #pragma unroll
-  for (int i = 0; i < K_UNIF; ++i) {
-    if (e0 + i < n) {
-      a.out[e0 + i] = r[i];
-      if (a.U && !need) a.U[e0 + i] = u[i];
+    for (int i = 0; i < K_UNIF; ++i)
+      if (e0 + i < n) a.out[e0 + i] = r[i];
+  }
+  if (a.U && !need) {
+    if (e0 + K_UNIF <= n && vec_ok(a.U + e0)) {
+      store_k(a.U + e0, u);
+    } else {
+#pragma unroll
+      for (int i = 0; i < K_UNIF; ++i)
+        if (e0 + i < n) a.U[e0 + i] = u[i];
     }
   }
   __syncthreads();

@@ -565,6 +565,10 @@ const char* dr_strerror(int code) {
   }
 }
 
+int dr_stream_synchronize(void* stream) {
+  return cudaStreamSynchronize((cudaStream_t)stream) == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
 int dr_device_accessible(const void* p) {
   cudaPointerAttributes a;
   if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {

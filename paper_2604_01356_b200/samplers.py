@@ -196,9 +196,8 @@ def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = N
 _status_cache: dict[int, torch.Tensor] = {}
 
 
-def _status_buf() -> torch.Tensor:
+def _status_buf(s: int) -> torch.Tensor:
     """A per-stream status word the kernels overwrite (no per-call zeroing)."""
-    s = _lib.stream_handle()
     t = _status_cache.get(s)
     if t is None:
         t = torch.empty(1, dtype=torch.int32, device=_lib.device())
@@ -209,10 +208,9 @@ def _status_buf() -> torch.Tensor:
 _scratch_u: dict[int, torch.Tensor] = {}
 
 
-def _scratch_uniforms(n: int) -> torch.Tensor:
+def _scratch_uniforms(n: int, s: int) -> torch.Tensor:
     """Per-stream device scratch for U when the caller does not ask for it
     (stream-ordered reuse is safe: every use is on the same stream)."""
-    s = _lib.stream_handle()
     t = _scratch_u.get(s)
     if t is None or t.numel() < n:
         t = torch.empty(max(n, 1024), dtype=torch.float64, device=_lib.device())
@@ -230,14 +228,14 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
         res = _match(kind, U, table, check=False, mode=mode)
         return res if device else res.cpu().numpy()
     L = _lib.lib()
+    s = _lib.stream_handle()
     to_host = out is None and not device
     if out is None:
         out = empty_i64(n) if device else host_result_i64(n)
-    U = _scratch_uniforms(n) if U is None else U
-    st = _status_buf()
-    ws, wsb = _lib.workspace(L.dr_workspace_bytes(_lib.OP_SORTED, 0, n, 0))
+    U = _scratch_uniforms(n, s) if U is None else U
+    st = _status_buf(s)
+    ws, wsb = _lib.workspace(_lib.workspace_bytes(_lib.OP_SORTED, n), s)
     W = table.device_cum
-    s = _lib.stream_handle()
     if not isinstance(stream, (RngStream, DeviceRngStream)):
         # duck-typed host stream: its n+1 uniforms feed the same fused kernel
         raw, _ = to_device_f64(stream.uniforms(n + 1))
@@ -245,7 +243,7 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
                                   U.data_ptr(), out.data_ptr(), st.data_ptr(), _lib.DAC_MODES[mode], ws, wsb, s)
         _lib.check(rc, "dr_sample_dac_from")
         if to_host:
-            return finish_host(out)
+            return finish_host(out, s)
         return out if device else out.cpu().numpy()
     k0, k1, off, offd = _stream_args(stream, n + 1)
     if kind == "ccf":
@@ -256,7 +254,7 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
                              U.data_ptr(), out.data_ptr(), st.data_ptr(), _lib.DAC_MODES[mode], ws, wsb, s)
     _lib.check(rc, f"dr_sample_{kind}")
     if to_host:
-        return finish_host(out)
+        return finish_host(out, s)
     return out if device else out.cpu().numpy()
 
 
