@@ -208,7 +208,8 @@ def run_drs(args, rank, world, local_rank):
 
         step = eager_step
         fused = args.sampler == "dac" and args.mode != "merge" and M > 16 * N and (N + 1) <= 148 * 512
-        launches_per_step = {"binary": 1, "ccf": 3}.get(args.sampler, 1 if fused else 3)
+        # sorted uniforms = pass 1 + chain + pass 2 + finalize, then the search
+        launches_per_step = {"binary": 1, "ccf": 5}.get(args.sampler, 1 if fused else 5)
         if args.graph:
             # one sampler call captured once; the stream position lives on the
             # device, so every replay draws fresh uniforms
@@ -223,8 +224,6 @@ def run_drs(args, rank, world, local_rank):
             torch.cuda.current_stream().wait_stream(side)
             if args.sampler == "binary":
                 launches_per_step += 1  # the device-side stream advance
-            elif not fused:
-                launches_per_step += 1
 
             def step():
                 graph.replay()
@@ -283,6 +282,29 @@ def run_drs(args, rank, world, local_rank):
         k_ms.append(a.elapsed_time(b))
     kernel_ms = statistics.median(k_ms)
 
+    # ---- K1 on its own: build_weight_table from device-resident raw weights
+    # (16 M algorithmic bytes -- read w, write W)
+    table_build = None
+    if cfg in ("c1", "c2", "c3") or (cfg == "c5" and world == 1):
+        w_dev = torch.from_numpy(w_host).to(dev)
+        drs.build_weight_table(w_dev, check=False)
+        tb_ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            l2_flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            drs.build_weight_table(w_dev, check=False)
+            b.record(s)
+            torch.cuda.synchronize()
+            tb_ms.append(a.elapsed_time(b))
+        del w_dev
+        tbm = statistics.median(tb_ms)
+        M_ = c["M"]
+        table_build = {"ms": tbm, "GB/s": 16 * M_ / (tbm * 1e-3) / 1e9,
+                       "frac": 16 * M_ / (tbm * 1e-3) / 1e9 / peak_hbm()[0],
+                       "algorithmic_bytes": 16 * M_, "launches": 3,
+                       "note": "read w + write W (the index levels are extra); passes read w twice"}
+
     # ---- end to end through the public API, host result (and host weights for c4)
     e2e = None
     if e2e_step is not None:
@@ -330,6 +352,7 @@ def run_drs(args, rank, world, local_rank):
                      "algorithmic_bytes_per_launch": alg_bytes},
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
+        "table_build": table_build,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
         "timing": "CUDA-graph replay of one sampler call (device-resident stream position)"

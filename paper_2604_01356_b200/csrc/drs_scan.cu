@@ -270,29 +270,34 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
     double v = fmin(__ddiv_rn(S, T), 1.0);
     if (j == n - 1) v = 1.0;
     chunk[i] = v;
-    if (j < n && ((j & (FANOUT - 1)) == FANOUT - 1 || j == n - 1)) {
-      int64_t span = FANOUT;
-      for (int k = 1; k <= d.levels; ++k, span *= FANOUT) {
-        const bool edge = ((j + 1) % span) == 0;
-        if (!edge && j != n - 1) break;
-        idx[d.off[k] + j / span] = v;
-        if (j == n - 1) {
-          const int64_t padded = cdiv(d.n[k], FANOUT) * FANOUT;
-          for (int64_t p = d.n[k]; p < padded; ++p) idx[d.off[k] + p] = dinf();
-        }
-      }
-    }
   }
   fence_proxy_async_smem();
   __syncthreads();
   const int64_t len_even = len & ~(int64_t)1;
+  const int64_t j0 = t * TS;
   if (threadIdx.x == 0) {
-    if (len_even > 0) {
-      bulk_s2g(W + t * TS, sm, (uint32_t)(len_even * 8));
-      bulk_commit_wait();
-    }
-    if (len & 1) W[t * TS + len - 1] = sm[len - 1];
+    if (len_even > 0) bulk_s2g(W + j0, sm, (uint32_t)(len_even * 8));
+    if (len & 1) W[j0 + len - 1] = sm[len - 1];
   }
+  if (!RAW) {
+    // index entries ending in this tile, written cooperatively: level k holds
+    // W at every 16^k-block end (the last block ends at n-1), padded with +inf
+    static_assert(FANOUT == 16, "index levels use shifts by 4 bits per level");
+    const int64_t jl = j0 + len - 1;
+    for (int k = 1, sh = 4; k <= d.levels; ++k, sh += 4) {
+      const int64_t m0 = (j0 + 1 + ((int64_t)1 << sh) - 1) >> sh;  // (m0 + 1) << sh > j0: m0 - 1 ends at/after j0
+      const int64_t m1 = (jl + 1) >> sh;                             // blocks ending at or before jl
+      for (int64_t m = m0 - 1 + threadIdx.x; m < m1; m += THREADS)
+        if (m >= 0) idx[d.off[k] + m] = sm[((m + 1) << sh) - 1 - j0];
+      if (jl == n - 1) {  // the last, possibly partial, block and the padding
+        const int64_t mlast = (n - 1) >> sh;
+        const int64_t padded = cdiv(d.n[k], FANOUT) * FANOUT;
+        for (int64_t p = mlast + threadIdx.x; p < padded; p += THREADS)
+          idx[d.off[k] + p] = (p == mlast) ? sm[len - 1] : dinf();
+      }
+    }
+  }
+  if (threadIdx.x == 0 && len_even > 0) bulk_commit_wait();
   (void)status_out;
   (void)total_out;
 }
