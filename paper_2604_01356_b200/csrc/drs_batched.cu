@@ -54,28 +54,6 @@ __device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, dou
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
 }
 
-// the chained in-tile fold of dr_build_table / dr_sorted_uniforms
-__device__ __forceinline__ double tile_fold(double tau, double* s_g, double& Q, double& R) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc = 0.0;
-  Q = 0.0;
-#pragma unroll
-  for (int k = 0; k < LANES; ++k) {
-    Q = (lane == k) ? acc : Q;
-    acc = __dadd_rn(acc, __shfl_sync(FULL, tau, k));
-  }
-  if (lane == 0) s_g[warp] = acc;
-  __syncthreads();
-  double r = 0.0;
-  R = 0.0;
-#pragma unroll
-  for (int q = 0; q < WARPS; ++q) {
-    R = (q == warp) ? r : R;
-    r = __dadd_rn(r, s_g[q]);
-  }
-  return r;
-}
-
 // valid weight <=> 0 <= x < inf (-0.0 included, NaN excluded); screened from
 // the high word: any sign bit (exact re-check follows) or an all-ones exponent
 __device__ __forceinline__ void track_hi(double x, uint32_t& any_sign, uint32_t& max_mag) {
@@ -99,9 +77,9 @@ struct BatchedArgs {
 __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ double s_g[WARPS];   // warp totals of the table tile
+  __shared__ FoldSmem fst;        // fold of the table tile
+  __shared__ FoldSmem fsu;        // fold of a uniform tile
   __shared__ double s_R[WARPS];   // warp bases R of the table tile
-  __shared__ double s_gu[WARPS];  // warp totals of a uniform tile
   __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
   __shared__ double s_Au[MAX_UT];
   __shared__ unsigned long long s_min;
@@ -133,6 +111,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   for (int i = len + threadIdx.x; i < TS_TABLE; i += THREADS) sw[i] = 0.0;  // tile padding
   const uint64_t k0 = a.keys[3 * f], k1 = a.keys[3 * f + 1], off = a.keys[3 * f + 2];
   __syncthreads();
+  STAMP(0);
   // first half of a split cluster barrier: peers may store into this CTA's
   // shared memory only once every CTA of the cluster is running
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
@@ -166,12 +145,12 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
 #pragma unroll
       for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
       double Q, R;
-      const double A = tile_fold(sc[K_UNIF - 1], s_gu, Q, R);
+      const double A = block_fold(sc[K_UNIF - 1], fsu, Q, R);
       if (threadIdx.x == 0) s_Au[t] = A;
 #pragma unroll
       for (int i = 0; i < K_UNIF; ++i)
         if (e0 + i < ne) su[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
-      __syncthreads();  // s_gu reuse
+      __syncthreads();  // fsu reuse
     }
     if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
     double Pu[MAX_UT];
@@ -211,7 +190,9 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   }
 
   // ---- 2. the table sweep over this CTA's tile
+  STAMP(1);
   if (tma) mbar_wait(&bar, 0);
+  STAMP(2);
   uint32_t any_sign = 0, max_mag = 0;
   const int c0 = threadIdx.x * K_TABLE;
   double* chunk = sw + c0;
@@ -237,11 +218,12 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   if (any_sign & 0x80000000u)         // a sign bit: re-check the raw weights (-0.0 is valid)
     for (int i = 0; i < K_TABLE && c0 + i < len; ++i) bad |= !(wt[c0 + i] >= 0.0);
   double Q, R;
-  const double A = tile_fold(s, s_g, Q, R);
+  const double A = block_fold(s, fst, Q, R);
   sQ[threadIdx.x] = Q;
   if (lane == 0) s_R[warp] = R;
   if (bad) s_bad = 1;
 
+  STAMP(3);
   // ---- 3. exchange the tile totals through distributed shared memory
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   if (threadIdx.x == 0)
@@ -253,6 +235,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
     T = __dadd_rn(T, s_A[q]);
   }
   const double Pnext = __dadd_rn(Pr, s_A[r]);  // == S at the tile's last entry
+  STAMP(4);
   if (threadIdx.x == 0) {
     int st = s_bad ? DRS_ST_INVALID_WEIGHT : 0;
     if (r == 0) {
@@ -313,6 +296,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
       if (a.Uout) a.Uout[f * Nf + i] = x;
     }
   }
+  STAMP(5);
   if (a.Wout) {
     for (int j = threadIdx.x; j < len; j += THREADS) {
       const int c = j / K_TABLE;
@@ -325,6 +309,12 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
 }  // namespace drs
 
 using namespace drs;
+
+#ifdef DRS_PHASE_TIMING
+extern "C" int dr_debug_phase_times_batched(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64_t Nf,
                                    uint64_t* keys, int32_t advance, double* W, double* U,

@@ -37,24 +37,6 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
 int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
                  int64_t* out, cudaStream_t st);
 
-#ifdef DRS_PHASE_TIMING
-// phase timestamps (profiling builds only): dbg[cta * 16 + phase] = %globaltimer
-__device__ unsigned long long g_phase[4096 * 16];
-#define STAMP(ph)                                                             \
-  do {                                                                        \
-    __syncthreads();                                                          \
-    if (threadIdx.x == 0) {                                                   \
-      unsigned long long tt_;                                                 \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_));                \
-      g_phase[blockIdx.x * 16 + (ph)] = tt_;                                  \
-    }                                                                         \
-  } while (0)
-#else
-#define STAMP(ph) \
-  do {            \
-  } while (0)
-#endif
-
 constexpr int SIDX_CAP = 24576;
 constexpr int FUSED_MAX_TILES = 160;   // >= co-resident CTAs (148 SMs x 1); <= FLAG_CAP
 #ifndef DRS_L2_PREFETCH_MB
@@ -190,27 +172,6 @@ __device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen) {
   __syncthreads();
 }
 
-__device__ __forceinline__ double chain_fold_f(double tau, double* s_g, double& Q, double& R) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc = 0.0;
-  Q = 0.0;
-#pragma unroll
-  for (int k = 0; k < LANES; ++k) {
-    if (lane == k) Q = acc;
-    acc = __dadd_rn(acc, __shfl_sync(FULL, tau, k));
-  }
-  if (lane == 0) s_g[warp] = acc;
-  __syncthreads();
-  double r = 0.0;
-  R = 0.0;
-#pragma unroll
-  for (int v = 0; v < WARPS; ++v) {
-    if (v == warp) R = r;
-    r = __dadd_rn(r, s_g[v]);
-  }
-  return r;
-}
-
 struct FusedArgs {
   const double* W;
   const double* idx;
@@ -229,7 +190,7 @@ struct FusedArgs {
 __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(128) double sidx[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ double s_g[WARPS];
+  __shared__ FoldSmem fs;
   __shared__ double s_last[WARPS];
   __shared__ double s_C, s_P, s_total;
   __shared__ unsigned long long s_min;
@@ -288,7 +249,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
   atomicMin(&s_min, mn);
   double Q, R;
-  const double A = chain_fold_f(sc[K_UNIF - 1], s_g, Q, R);
+  const double A = block_fold(sc[K_UNIF - 1], fs, Q, R);
   STAMP(2);
   STAMP(3);
   if (threadIdx.x == 0) {

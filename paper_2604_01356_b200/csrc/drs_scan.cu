@@ -57,30 +57,6 @@ __global__ void k_ws_init(ScanHdr* h) {
   h->total = 0.0;
 }
 
-// --------------------------------------------------------- tile chain ----
-// Q: fold of previous lane-chunk totals in the warp; R: fold of previous warp
-// totals in the tile; returns A = tile total.  Serial folds, starting at 0.0.
-__device__ __forceinline__ double chain_fold(double tau, double* s_g, double& Q, double& R) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double acc = 0.0;
-  Q = 0.0;
-#pragma unroll
-  for (int k = 0; k < LANES; ++k) {
-    if (lane == k) Q = acc;
-    acc = __dadd_rn(acc, __shfl_sync(FULL, tau, k));
-  }
-  if (lane == 0) s_g[warp] = acc;
-  __syncthreads();
-  double r = 0.0;
-  R = 0.0;
-#pragma unroll
-  for (int v = 0; v < WARPS; ++v) {
-    if (v == warp) R = r;
-    r = __dadd_rn(r, s_g[v]);
-  }
-  return r;
-}
-
 // The tile chain: one CTA folds the nt tile totals.  Thread g folds group g
 // serially (D_t, exclusive) and leaves the group total; thread 0 then folds
 // the group totals serially (C_g, exclusive) and writes T = C_ng.  It also
@@ -205,7 +181,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
                                                          ScanWS ws) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ double s_g[WARPS];
+  __shared__ FoldSmem fs;
   const int64_t t = blockIdx.x;
   const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
   const int c0 = threadIdx.x * K_TABLE;
@@ -226,7 +202,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
   if (any_sign & 0x80000000u)
     for (int i = 0; i < K_TABLE; ++i) bad |= !(chunk[i] >= 0.0);
   double Q, R;
-  const double A = chain_fold(s, s_g, Q, R);
+  const double A = block_fold(s, fs, Q, R);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.hdr->status, (uint32_t)DRS_ST_INVALID_WEIGHT);
   if (threadIdx.x == 0) ws.agg[t] = A;
   (void)len;
@@ -242,7 +218,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
                                                          int32_t* status_out, double* total_out) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ double s_g[WARPS];
+  __shared__ FoldSmem fs;
   constexpr int64_t TS = (int64_t)THREADS * K_TABLE;
   const int64_t t = blockIdx.x;
   const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
@@ -252,7 +228,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
 #pragma unroll
   for (int i = 1; i < K_TABLE; ++i) s = __dadd_rn(s, chunk[i]);
   double Q, R;
-  chain_fold(s, s_g, Q, R);
+  block_fold(s, fs, Q, R);
   const double C = ws.grp[t / GROUP_TILES], D = ws.incl[t];
   const double T = ws.hdr->total;
   const int64_t jb = t * TS + (int64_t)(warp * LANES + lane) * K_TABLE;
@@ -314,7 +290,7 @@ __device__ __forceinline__ unsigned long long zmin_key(double z) {
 // total to agg[t]; the spacing minimum to the header.
 template <class Src>
 __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, ScanWS ws, double* __restrict__ Z) {
-  __shared__ double s_g[WARPS];
+  __shared__ FoldSmem fs;
   __shared__ unsigned long long s_min;
   __shared__ uint64_t s_words[Src::SMEM_WORDS];
   if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
@@ -333,7 +309,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
   if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
   double Q, R;
-  const double A = chain_fold(sc[K_UNIF - 1], s_g, Q, R);  // contains __syncthreads
+  const double A = block_fold(sc[K_UNIF - 1], fs, Q, R);  // contains __syncthreads
   if (threadIdx.x == 0) {
     ws.agg[t] = A;
     ws.incl[t] = __longlong_as_double((long long)s_min);  // folded by k_chain_groups
