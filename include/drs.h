@@ -199,6 +199,26 @@ int dr_shard_match(const double *W, const double *idx, int64_t Mg, int64_t shard
                    const double *U, int64_t N, const int64_t *range, int64_t *out,
                    void *stream);
 
+/* --- either side of the path --- */
+
+/* The step after resampling: out[i][0..d) =
+ * states[idx[i] / divisor][0..d) for a row-major states[K][d] (divisor = N_Y
+ * maps an EnGMF component index (particle, center) to its particle).
+ * status gets OUT_OF_SUPPORT for an index outside [0, K*divisor). */
+int dr_gather_rows(const double *states, int64_t K, int64_t d, const int64_t *idx, int64_t N,
+                   int64_t divisor, double *out, int32_t *status, void *stream);
+
+/* np.bincount(idx, minlength=M) (bench.py:241): counts[M] (zeroed here);
+ * status gets OUT_OF_SUPPORT for an index outside [0, M). */
+int dr_histogram(const int64_t *idx, int64_t N, int64_t M, uint64_t *counts, int32_t *status,
+                 void *stream);
+
+/* chi_square_statistic(counts, n * table.weights()) (bench.py:221-225,
+ * cdf.py:51-53) with a fixed reduction order; *out on the device. */
+size_t dr_chi_square_workspace(int64_t M);
+int dr_chi_square(const uint64_t *counts, const double *W, int64_t M, int64_t n, double *out, void *ws,
+                  size_t ws_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

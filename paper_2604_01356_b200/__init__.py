@@ -26,6 +26,7 @@ from .samplers import (
     warm_kernels,
 )
 from .sharded import ShardedWeightTable, build_sharded_table, sharded_dac_sampler
+from .verify import chi_square_statistic, gather_states, histogram, verify_statistics
 
 __all__ = [
     "RngStream",
@@ -48,6 +49,10 @@ __all__ = [
     "ShardedWeightTable",
     "build_sharded_table",
     "sharded_dac_sampler",
+    "gather_states",
+    "histogram",
+    "chi_square_statistic",
+    "verify_statistics",
 ]
 
 __version__ = "0.1.0"

@@ -1,0 +1,140 @@
+// drs_extra.cu -- the steps either side of the resampling path.
+//
+//   gather          the step after resampling: particle states by index
+//                   ("trivial"; EnGMF rows of d = 40 fp64,
+//                   weightgen.py:37), out[i] = states[idx[i] / divisor].
+//   histogram       np.bincount(indices, minlength=M) (bench.py:241) on the
+//                   device: warp-aggregated atomics (equal indices of a warp
+//                   -- sorted samplers produce long runs -- add once).
+//   chi_square      chi_square_statistic(counts, n * weights) (bench.py:221-225,
+//                   expected from table.weights() = diff(W, prepend 0),
+//                   cdf.py:51-53), reduced deterministically (fixed tree).
+#include "drs_common.cuh"
+
+namespace drs {
+
+static int launch_rc_x() {
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
+// one warp per output row; 16-byte accesses when rows are 16-byte aligned
+__global__ void __launch_bounds__(256) k_gather_rows(const double* __restrict__ states, int64_t K, int64_t d,
+                                                     const int64_t* __restrict__ idx, int64_t N,
+                                                     int64_t divisor, double* __restrict__ out,
+                                                     int32_t* status, int vec2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < N; i += warps) {
+    const int64_t src = __ldg(idx + i) / divisor;
+    if (src < 0 || src >= K) {
+      if (lane == 0) atomicOr(status, DRS_ST_OUT_OF_SUPPORT);
+      continue;
+    }
+    const double* s = states + src * d;
+    double* o = out + i * d;
+    if (vec2) {
+      const double2* s2 = reinterpret_cast<const double2*>(s);
+      double2* o2 = reinterpret_cast<double2*>(o);
+      for (int64_t k = lane; k < d / 2; k += 32) o2[k] = __ldg(s2 + k);
+    } else {
+      for (int64_t k = lane; k < d; k += 32) o[k] = __ldg(s + k);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_histogram(const int64_t* __restrict__ idx, int64_t N, int64_t M,
+                                                   unsigned long long* __restrict__ counts, int32_t* status) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < N; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const int64_t j = (i < N) ? __ldg(idx + i) : -1;
+    const bool ok = (i < N) && j >= 0 && j < M;
+    if (i < N && !ok) atomicOr(status, DRS_ST_OUT_OF_SUPPORT);
+    const unsigned act = __ballot_sync(FULL, ok);
+    if (!ok) continue;
+    // lanes holding the same index: the lowest adds the group size
+    const unsigned peers = __match_any_sync(act, (unsigned long long)j);
+    if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(counts + j, (unsigned long long)__popc(peers));
+  }
+}
+
+// per-bin Pearson terms, then a fixed two-level tree: 256-thread blocks over
+// contiguous bins, block partials summed in block order by one thread
+constexpr int CHI_THREADS = 256;
+
+__global__ void __launch_bounds__(CHI_THREADS) k_chi_partial(const unsigned long long* __restrict__ counts,
+                                                             const double* __restrict__ W, int64_t M,
+                                                             double n, double* __restrict__ partial) {
+  __shared__ double red[CHI_THREADS];
+  const int64_t per = (int64_t)gridDim.x;
+  double acc = 0.0;
+  // block b takes bins [b*M/g, (b+1)*M/g); thread t folds its strided bins in order
+  const int64_t b0 = M * blockIdx.x / per, b1 = M * (blockIdx.x + 1) / per;
+  for (int64_t j = b0 + threadIdx.x; j < b1; j += CHI_THREADS) {
+    const double wj = (j == 0) ? W[0] : __dsub_rn(W[j], W[j - 1]);
+    const double e = __dmul_rn(n, wj);
+    const double dlt = __dsub_rn((double)counts[j], e);
+    acc = __dadd_rn(acc, __ddiv_rn(__dmul_rn(dlt, dlt), e));
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = CHI_THREADS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + s]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial[blockIdx.x] = red[0];
+}
+
+__global__ void k_chi_final(const double* __restrict__ partial, int nb, double* out) {
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s = __dadd_rn(s, partial[b]);
+  *out = s;
+}
+
+}  // namespace drs
+
+using namespace drs;
+
+extern "C" {
+
+int dr_gather_rows(const double* states, int64_t K, int64_t d, const int64_t* idx, int64_t N, int64_t divisor,
+                   double* out, int32_t* status, void* stream) {
+  if (K < 1 || d < 1 || N < 0 || divisor < 1 || !status || (N > 0 && (!states || !idx || !out)))
+    return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
+  if (N == 0) return DRS_OK;
+  const int vec2 = ((d & 1) == 0) && ((((uintptr_t)states) | ((uintptr_t)out)) & 15) == 0;
+  const int64_t warps = N < 148 * 64 ? N : 148 * 64;
+  k_gather_rows<<<(unsigned)cdiv(warps, 8), 256, 0, st>>>(states, K, d, idx, N, divisor, out, status, vec2);
+  return launch_rc_x();
+}
+
+int dr_histogram(const int64_t* idx, int64_t N, int64_t M, uint64_t* counts, int32_t* status, void* stream) {
+  if (N < 0 || M < 1 || !counts || !status || (N > 0 && !idx)) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
+  if (cudaMemsetAsync(counts, 0, sizeof(uint64_t) * (size_t)M, st) != cudaSuccess) return DRS_ERR_LAUNCH;
+  if (N == 0) return DRS_OK;
+  const int64_t blocks = cdiv(N, 256) < 148 * 8 ? cdiv(N, 256) : 148 * 8;
+  k_histogram<<<(unsigned)blocks, 256, 0, st>>>(idx, N, M, (unsigned long long*)counts, status);
+  return launch_rc_x();
+}
+
+size_t dr_chi_square_workspace(int64_t M) {
+  (void)M;
+  return sizeof(double) * 1024;
+}
+
+int dr_chi_square(const uint64_t* counts, const double* W, int64_t M, int64_t n, double* out, void* ws,
+                  size_t ws_bytes, void* stream) {
+  if (M < 1 || n < 0 || !counts || !W || !out || !ws || ws_bytes < dr_chi_square_workspace(M)) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nb = (int)(cdiv(M, 4096) < 1024 ? cdiv(M, 4096) : 1024);
+  k_chi_partial<<<nb, CHI_THREADS, 0, st>>>((const unsigned long long*)counts, W, M, (double)n, (double*)ws);
+  k_chi_final<<<1, 1, 0, st>>>((const double*)ws, nb, out);
+  return launch_rc_x();
+}
+
+}  // extern "C"
