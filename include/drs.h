@@ -88,6 +88,14 @@ int64_t dr_index_entries(int64_t M);
 int dr_build_table(const double *w, int64_t M, double *W, double *idx, int32_t *status,
                    void *ws, size_t ws_bytes, void *stream);
 
+/* The fused weight producer: the table of
+ * w = exp(logw - max(logw)) -- weightgen.py:152-153 (engmf_weights' shift and
+ * exp) followed by build_weight_table (cdf.py:59-89) -- without writing w:
+ * a max reduction, then both table passes form w in shared memory with the
+ * device exp (oracle/drs_ref_exp twin).  A NaN log-weight gives INVALID_WEIGHT. */
+int dr_build_table_log(const double *logw, int64_t M, double *W, double *idx, int32_t *status,
+                       void *ws, size_t ws_bytes, void *stream);
+
 /* WeightTable.__init__ validation (cdf.py:31-42) of a caller-supplied
  * cumulative array: NONFINITE / DECREASING / TOP_NOT_ONE. */
 int dr_validate_table(const double *W, int64_t M, int32_t *status, void *stream);

@@ -125,6 +125,56 @@ double drs_ref_log(double x) {
   return s2 + small;
 }
 
+/* exp with the device's operation sequence (drs_common.cuh:dexp) */
+double drs_ref_exp(double x) {
+  if (x != x) return x;
+  if (x > 709.782712893384) return INFINITY;
+  if (x < -745.1332191019412) return 0.0;
+  const double kd = rint(x * 0x1.71547652b82fep+0);
+  double r = fma(-kd, 0x1.62e42fefa39efp-1, x);
+  r = fma(-kd, 0x1.abc9e3b39803fp-56, r);
+  double p = 1.0 / 6227020800.0; /* e^r: degree-13 Taylor polynomial, Horner with FMAs */
+  p = fma(p, r, 1.0 / 479001600.0);
+  p = fma(p, r, 1.0 / 39916800.0);
+  p = fma(p, r, 1.0 / 3628800.0);
+  p = fma(p, r, 1.0 / 362880.0);
+  p = fma(p, r, 1.0 / 40320.0);
+  p = fma(p, r, 1.0 / 5040.0);
+  p = fma(p, r, 1.0 / 720.0);
+  p = fma(p, r, 1.0 / 120.0);
+  p = fma(p, r, 1.0 / 24.0);
+  p = fma(p, r, 1.0 / 6.0);
+  p = fma(p, r, 0.5);
+  p = fma(p, r, 1.0);
+  p = fma(p, r, 1.0);
+  const int k = (int)kd;
+  if (k > 1023) return (p * 2.0) * bitsd((uint64_t)(1023 + 1023) << 52);
+  if (k >= -1022) return p * bitsd((uint64_t)(k + 1023) << 52);
+  return (p * bitsd((uint64_t)(k + 54 + 1023) << 52)) * 0x1.0p-54;
+}
+
+void drs_ref_exp_array(const double *x, int64_t n, double *y) {
+  for (int64_t i = 0; i < n; ++i) y[i] = drs_ref_exp(x[i]);
+}
+
+/* build_weight_table(np.exp(logw - logw.max())) (weightgen.py:152-153 +
+ * cdf.py:59-89) with the device exp and association; a NaN log-weight makes
+ * the max NaN and every weight NaN ("invalid weight"). */
+int drs_ref_build_table_log(const double *lw, int64_t M, double *W) {
+  double mx = -INFINITY;
+  int nan = 0;
+  for (int64_t i = 0; i < M; ++i) {
+    if (lw[i] != lw[i]) nan = 1;
+    else if (lw[i] > mx) mx = lw[i];
+  }
+  if (nan) mx = NAN;
+  double *w = (double *)malloc(sizeof(double) * (size_t)M);
+  for (int64_t i = 0; i < M; ++i) w[i] = drs_ref_exp(lw[i] - mx);
+  const int st = drs_ref_build_table(w, M, W);
+  free(w);
+  return st;
+}
+
 void drs_ref_neglog_array(const double *u, int64_t n, double *z) {
   for (int64_t i = 0; i < n; ++i) z[i] = -drs_ref_log(u[i]);
 }

@@ -57,6 +57,9 @@ void drs_ref_neglog_array(const double *u, int64_t n, double *z);
 
 /* ---- device-association scans ---- */
 void drs_ref_chain_scan(const double *x, int64_t n, int K, double *S, double *total);
+double drs_ref_exp(double x);
+void drs_ref_exp_array(const double *x, int64_t n, double *y);
+int drs_ref_build_table_log(const double *lw, int64_t M, double *W);
 int drs_ref_build_table(const double *w, int64_t M, double *W);
 int drs_ref_sorted_from_z(const double *z, int64_t n, double *U);
 int drs_ref_sorted_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, double *U);

@@ -29,6 +29,9 @@ _PROTOS = {
     "drs_ref_neglog_array": (None, [_P, _I64, _P]),
     "drs_ref_chain_scan": (None, [_P, _I64, _INT, _P, _P]),
     "drs_ref_build_table": (_INT, [_P, _I64, _P]),
+    "drs_ref_exp": (_D, [_D]),
+    "drs_ref_exp_array": (None, [_P, _I64, _P]),
+    "drs_ref_build_table_log": (_INT, [_P, _I64, _P]),
     "drs_ref_sorted_from_z": (_INT, [_P, _I64, _P]),
     "drs_ref_sorted_uniforms": (_INT, [_U64, _U64, _U64, _I64, _P]),
     "drs_ref_sorted_uniforms_from": (_INT, [_P, _I64, _P]),
@@ -235,3 +238,17 @@ def port_batched_throughput(w, Nf, threads, reps, k0, k1):
     w = _f64(w)
     B, Mf = w.shape
     return float(lib().drs_port_batched_throughput(_p(w), B, Mf, int(Nf), int(threads), int(reps), k0, k1))
+
+
+def exp(x):
+    x = _f64(x)
+    y = np.empty_like(x)
+    lib().drs_ref_exp_array(_p(x), x.size, _p(y))
+    return y
+
+
+def build_table_log(lw):
+    lw = _f64(lw)
+    W = np.empty_like(lw)
+    st = lib().drs_ref_build_table_log(_p(lw), lw.size, _p(W))
+    return W, int(st)

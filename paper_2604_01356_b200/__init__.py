@@ -13,7 +13,7 @@ over several GPUs with a single all-gather of shard totals).
 """
 
 from .batched import BatchedStreams, resample_batched
-from .cdf import WeightTable, build_weight_table, upper_bound_search
+from .cdf import WeightTable, build_weight_table, build_weight_table_from_log, upper_bound_search
 from .randkit import DeviceRngStream, RngStream, sorted_uniforms, uniform_open
 from .samplers import (
     OpStats,
@@ -35,6 +35,7 @@ __all__ = [
     "sorted_uniforms",
     "WeightTable",
     "build_weight_table",
+    "build_weight_table_from_log",
     "upper_bound_search",
     "OpStats",
     "linear_oracle",

@@ -52,6 +52,7 @@ _PROTOS = {
     "dr_workspace_init": (_int, [_c_void_p, _size, _c_void_p]),
     "dr_index_entries": (_i64, [_i64]),
     "dr_build_table": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_build_table_log": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "dr_validate_table": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_build_index": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_uniforms": (_int, [_u64, _u64, _u64, _i64, _c_void_p, _c_void_p]),

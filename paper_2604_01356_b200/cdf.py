@@ -16,7 +16,7 @@ import torch
 from . import _lib
 from ._tensors import is_device_tensor, read_status, status_word, to_device_f64
 
-__all__ = ["WeightTable", "build_weight_table", "upper_bound_search"]
+__all__ = ["WeightTable", "build_weight_table", "build_weight_table_from_log", "upper_bound_search"]
 
 
 def _raise_build_status(st: int) -> None:
@@ -152,6 +152,43 @@ def build_weight_table(raw_weights, *, check: bool = True) -> WeightTable:
     _lib.check(
         L.dr_build_table(w.data_ptr(), m, W.data_ptr(), _ptr(idx), st.data_ptr(), ws, wsb, _lib.stream_handle()),
         "dr_build_table",
+    )
+    if check:
+        _raise_build_status(read_status(st))
+    return WeightTable(None, _built=(W, idx))
+
+
+def build_weight_table_from_log(log_weights, *, check: bool = True) -> WeightTable:
+    """The table of ``exp(log_weights - log_weights.max())`` in one device pipeline.
+
+    The fused weight producer of SURVEY 8(f): the reference's EnGMF field
+    shifts its log-weights by the maximum and exponentiates
+    (weightgen.py:152-153) before ``build_weight_table`` (cdf.py:59-89); here
+    a max reduction and the two table passes form the weights in shared
+    memory (device exp, within 1 ulp of np.exp), so w is never written.
+    Errors as ``build_weight_table`` (a NaN log-weight is an "invalid weight").
+    """
+    if is_device_tensor(log_weights):
+        if log_weights.ndim != 1 or log_weights.numel() == 0:
+            raise ValueError("empty distribution")
+        lw = log_weights
+    else:
+        a = np.asarray(log_weights, dtype=np.float64)
+        if a.ndim != 1 or a.size == 0:
+            raise ValueError("empty distribution")
+        lw = a
+    lw, _ = to_device_f64(lw)
+    if lw.data_ptr() % 16:
+        lw = lw.clone()
+    m = lw.numel()
+    L = _lib.lib()
+    W = torch.empty(m, dtype=torch.float64, device=_lib.device())
+    idx = _new_index(m)
+    st = status_word()
+    ws, wsb = _lib.workspace(L.dr_workspace_bytes(_lib.OP_TABLE, m, 0, 0))
+    _lib.check(
+        L.dr_build_table_log(lw.data_ptr(), m, W.data_ptr(), _ptr(idx), st.data_ptr(), ws, wsb, _lib.stream_handle()),
+        "dr_build_table_log",
     )
     if check:
         _raise_build_status(read_status(st))

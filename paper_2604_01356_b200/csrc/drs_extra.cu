@@ -18,28 +18,22 @@ static int launch_rc_x() {
   return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 
-// one warp per output row; 16-byte accesses when rows are 16-byte aligned
-__global__ void __launch_bounds__(256) k_gather_rows(const double* __restrict__ states, int64_t K, int64_t d,
+// one thread per 16-byte (or 8-byte) element of the output: stores fully
+// coalesced, each source row read as one contiguous run
+template <typename V>
+__global__ void __launch_bounds__(256) k_gather_rows(const V* __restrict__ states, int64_t K, int64_t dv,
                                                      const int64_t* __restrict__ idx, int64_t N,
-                                                     int64_t divisor, double* __restrict__ out,
-                                                     int32_t* status, int vec2) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < N; i += warps) {
+                                                     int64_t divisor, V* __restrict__ out, int32_t* status) {
+  const int64_t total = N * dv;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t i = e / dv, k = e - i * dv;
     const int64_t src = __ldg(idx + i) / divisor;
     if (src < 0 || src >= K) {
-      if (lane == 0) atomicOr(status, DRS_ST_OUT_OF_SUPPORT);
+      if (k == 0) atomicOr(status, DRS_ST_OUT_OF_SUPPORT);
       continue;
     }
-    const double* s = states + src * d;
-    double* o = out + i * d;
-    if (vec2) {
-      const double2* s2 = reinterpret_cast<const double2*>(s);
-      double2* o2 = reinterpret_cast<double2*>(o);
-      for (int64_t k = lane; k < d / 2; k += 32) o2[k] = __ldg(s2 + k);
-    } else {
-      for (int64_t k = lane; k < d; k += 32) o[k] = __ldg(s + k);
-    }
+    out[e] = __ldg(states + src * dv + k);
   }
 }
 
@@ -105,9 +99,14 @@ int dr_gather_rows(const double* states, int64_t K, int64_t d, const int64_t* id
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
   if (N == 0) return DRS_OK;
-  const int vec2 = ((d & 1) == 0) && ((((uintptr_t)states) | ((uintptr_t)out)) & 15) == 0;
-  const int64_t warps = N < 148 * 64 ? N : 148 * 64;
-  k_gather_rows<<<(unsigned)cdiv(warps, 8), 256, 0, st>>>(states, K, d, idx, N, divisor, out, status, vec2);
+  const bool vec2 = ((d & 1) == 0) && ((((uintptr_t)states) | ((uintptr_t)out)) & 15) == 0;
+  const int64_t total = vec2 ? N * (d / 2) : N * d;
+  const int64_t blocks = cdiv(total, 256) < 148 * 16 ? cdiv(total, 256) : 148 * 16;
+  if (vec2)
+    k_gather_rows<double2><<<(unsigned)blocks, 256, 0, st>>>((const double2*)states, K, d / 2, idx, N, divisor,
+                                                             (double2*)out, status);
+  else
+    k_gather_rows<double><<<(unsigned)blocks, 256, 0, st>>>(states, K, d, idx, N, divisor, out, status);
   return launch_rc_x();
 }
 

@@ -51,7 +51,7 @@ __host__ inline ScanWS carve(void* ws, size_t ws_bytes) {
 }
 
 __global__ void k_ws_init(ScanHdr* h) {
-  h->done2 = 0;
+  h->done = 0;
   h->status = 0; h->nsites = 0; h->top = 0; h->bar_count = 0; h->bar_gen = 0;
   h->zmin_bits = 0x7FF0000000000000ULL;
   h->total = 0.0;
@@ -177,13 +177,85 @@ __device__ __forceinline__ int64_t stage_tile(const double* __restrict__ src, in
   return len;
 }
 
+// ------------------------------------------------- log-weight tables ----
+// max over the log-weights (order-independent, exact) with NaN propagation:
+// per-CTA maxima in agg[], the last CTA folds them into hdr->wmax.
+__device__ __forceinline__ unsigned long long ord_key(double x) {  // total order on non-NaN doubles
+  const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double ord_val(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : ~k));
+}
+
+__global__ void __launch_bounds__(256) k_max_logw(const double* __restrict__ lw, int64_t n, ScanWS ws) {
+  __shared__ unsigned long long s_key;
+  __shared__ int s_nan;
+  __shared__ bool s_last;
+  if (threadIdx.x == 0) { s_key = 0; s_nan = 0; }
+  __syncthreads();
+  unsigned long long key = 0;
+  bool nan = false;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double x = __ldg(lw + i);
+    if (x != x) nan = true;
+    else key = max(key, ord_key(x));
+  }
+  atomicMax(&s_key, key);
+  if (nan) s_nan = 1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ws.agg[blockIdx.x] = __longlong_as_double((long long)(s_nan ? ~0ULL : s_key));
+    __threadfence();
+    s_last = atomicAdd(&ws.hdr->done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long k = 0;
+    bool anynan = false;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      const unsigned long long v = (unsigned long long)__double_as_longlong(ld_relaxed_f64(&ws.agg[b]));
+      if (v == ~0ULL) anynan = true;
+      else k = max(k, v);
+    }
+    ws.hdr->wmax = anynan ? __longlong_as_double(0x7FF8000000000000LL) : ord_val(k);
+    ws.hdr->done = 0;
+  }
+}
+
+// the staged tile of log-weights -> w = exp(lw - max) in place (padding stays 0)
+__device__ __forceinline__ void exp_shift_tile(double* sm, int64_t len, double mx) {
+  const int c0 = threadIdx.x * K_TABLE;
+#pragma unroll 3
+  for (int i = 0; i < K_TABLE; ++i)
+    if (c0 + i < len) sm[c0 + i] = dexp(__dsub_rn(sm[c0 + i], mx));
+  __syncwarp();
+}
+
+// LOGW: the staged log-weights become w = exp(lw - max) in place and the
+// tile of w is stored to wout (the table buffer), which pass 2 then scans:
+// each exp is evaluated once
+template <bool LOGW>
 __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restrict__ w, int64_t n,
-                                                         ScanWS ws) {
+                                                         ScanWS ws, double* __restrict__ wout) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ FoldSmem fs;
   const int64_t t = blockIdx.x;
   const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
+  if (LOGW) {
+    exp_shift_tile(sm, len, ws.hdr->wmax);  // each thread transforms its own chunk
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int64_t j0 = t * (int64_t)THREADS * K_TABLE;
+      const int64_t le = len & ~(int64_t)1;
+      if (le > 0) bulk_s2g(wout + j0, sm, (uint32_t)(le * 8));
+      if (len & 1) wout[j0 + len - 1] = sm[len - 1];
+    }
+  }
   const int c0 = threadIdx.x * K_TABLE;
   const double* chunk = sm + c0;
   // valid weight <=> 0 <= x < inf: screened from the high words (integer
@@ -205,12 +277,12 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
   const double A = block_fold(s, fs, Q, R);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.hdr->status, (uint32_t)DRS_ST_INVALID_WEIGHT);
   if (threadIdx.x == 0) ws.agg[t] = A;
-  (void)len;
+  if (LOGW && threadIdx.x == 0) bulk_commit_wait();  // smem stays valid until the store has read it
 }
 
 // RAW = false: W = min(S/T, 1) with W[n-1] = 1 and the index levels (dr_build_table)
 // RAW = true:  the unnormalised local prefix S and *total_out = T (dr_shard_scan)
-template <bool RAW>
+template <bool RAW, bool LOGW>
 __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restrict__ w, int64_t n,
                                                          int64_t nt, ScanWS ws,
                                                          double* __restrict__ W,
@@ -222,6 +294,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
   constexpr int64_t TS = (int64_t)THREADS * K_TABLE;
   const int64_t t = blockIdx.x;
   const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
+  if (LOGW) exp_shift_tile(sm, len, ws.hdr->wmax);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* chunk = sm + (warp * LANES + lane) * K_TABLE;
   double s = chunk[0];
@@ -484,9 +557,10 @@ static bool g_attr_done = false;
 static void set_attrs() {
   if (g_attr_done) return;
   const int smem = THREADS * K_TABLE * 8;
-  cudaFuncSetAttribute(k_table_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_table_pass2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_table_pass2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_table_pass1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_table_pass1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_table_pass2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_table_pass2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   g_attr_done = true;
 }
 
@@ -595,9 +669,31 @@ int dr_build_table(const double* w, int64_t M, double* W, double* idx, int32_t* 
   const ScanWS s = carve(ws, ws_bytes);
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
-  k_table_pass1<<<(unsigned)nt, THREADS, smem, st>>>(w, M, s);
+  k_table_pass1<false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, s, nullptr);
   launch_chain(s, nt, 0, status, nullptr, st);
-  k_table_pass2<false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, nt, s, W, idx, d, status, nullptr);
+  k_table_pass2<false, false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, nt, s, W, idx, d, status, nullptr);
+  return launch_rc();
+}
+
+int dr_build_table_log(const double* logw, int64_t M, double* W, double* idx, int32_t* status, void* ws,
+                       size_t ws_bytes, void* stream) {
+  if (M < 1 || !logw || !W || !status || !ws) return DRS_ERR_ARG;
+  if (((uintptr_t)logw | (uintptr_t)W) & 15) return DRS_ERR_ALIGN;
+  const IndexDesc d = make_index_desc(M);
+  if (d.levels > 0 && !idx) return DRS_ERR_ARG;
+  const int64_t nt = cdiv(M, (int64_t)THREADS * K_TABLE);
+  if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
+  set_attrs();
+  const ScanWS s = carve(ws, ws_bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int smem = THREADS * K_TABLE * 8;
+  const int64_t mb = cdiv(M, 256 * 8);
+  const unsigned mgrid = (unsigned)(mb < nt ? (mb < 1 ? 1 : mb) : nt);  // partials fit in agg[nt]
+  k_max_logw<<<mgrid < 1184 ? mgrid : 1184, 256, 0, st>>>(logw, M, s);
+  k_table_pass1<true><<<(unsigned)nt, THREADS, smem, st>>>(logw, M, s, W);  // w -> W
+  launch_chain(s, nt, 0, status, nullptr, st);
+  k_table_pass2<false, false><<<(unsigned)nt, THREADS, smem, st>>>(W, M, nt, s, W, idx, d, status, nullptr);
   return launch_rc();
 }
 
@@ -613,9 +709,9 @@ int dr_shard_scan(const double* w_shard, int64_t Mg, double* S, double* Tg, int3
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
   const IndexDesc d = make_index_desc(Mg);
-  k_table_pass1<<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, s);
+  k_table_pass1<false><<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, s, nullptr);
   launch_chain(s, nt, 0, status, Tg, st);
-  k_table_pass2<true><<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, nt, s, S, nullptr, d, status, Tg);
+  k_table_pass2<true, false><<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, nt, s, S, nullptr, d, status, Tg);
   return launch_rc();
 }
 

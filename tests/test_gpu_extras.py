@@ -85,3 +85,34 @@ def test_cli_bench_writes_reference_schema(drs, tmp_path):
     lines = out.read_text().splitlines()
     assert lines[0] == "Ns,timesdcM1,timesccfM1,timesbM1,timesdcM10,timesccfM10,timesbM10"
     assert len(lines) == 3 and all(float(v) > 0 for v in lines[1].split(",")[1:])
+
+
+@pytest.mark.parametrize("M", [1, 2, 17, 8448, 8449, 300_001, 256 * 8448 + 5])
+def test_log_table_bit_exact_vs_oracle(drs, orc, M):
+    """max -> exp -> scan fused on the device == the oracle
+    twin bit for bit (W and the index), across tile and group boundaries."""
+    rng = np.random.default_rng(M)
+    lw = np.log(1 / 256) + np.log(rng.dirichlet(np.ones(64), size=max(1, M // 64 + 1)).ravel()[:M]) \
+        - 0.5 * rng.chisquare(6, size=M)
+    t = drs.build_weight_table_from_log(lw)
+    Wo, st = orc.build_table_log(lw)
+    assert st == 0
+    np.testing.assert_array_equal(t.cum, Wo)
+    if M > 16:
+        np.testing.assert_array_equal(t.device_index.cpu().numpy(), orc.build_index(Wo))
+    # the same table as build_weight_table of the device-exp weights
+    np.testing.assert_array_equal(drs.build_weight_table(orc.exp(lw - lw.max())).cum, Wo)
+    # and close to the reference pipeline np.exp + build_weight_table
+    Wp, _ = orc.port_build_table(np.exp(lw - lw.max()))
+    assert np.abs(t.cum - Wp).max() <= 1e-12
+
+
+def test_log_table_errors(drs):
+    with pytest.raises(ValueError, match="empty distribution"):
+        drs.build_weight_table_from_log(np.zeros(0))
+    with pytest.raises(ValueError, match="invalid weight"):
+        drs.build_weight_table_from_log(np.array([0.0, np.nan, 1.0]))
+    with pytest.raises(ValueError, match="invalid weight"):
+        drs.build_weight_table_from_log(np.array([0.0, np.inf]))
+    t = drs.build_weight_table_from_log(np.array([-np.inf, 0.0, -np.inf]))  # exp(-inf) = 0 weights
+    np.testing.assert_array_equal(t.cum, [0.0, 1.0, 1.0])

@@ -233,3 +233,37 @@ def test_chain_scan_group_boundaries_monotone(orc, K):
     assert tot == S[-1]
     ref = np.cumsum(x)
     assert np.abs(S - ref).max() <= 1e-12 * ref[-1]
+
+
+def test_device_exp_twin_within_one_ulp(orc):
+    """oracle/drs_ref_exp (the device exp's twin): <= 1 ulp from np.exp and
+    < 1 ulp from an extended-precision exp over the whole finite range."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.uniform(-745.0, 709.7, 400_000), rng.uniform(-1, 1, 100_000),
+                        -rng.exponential(40.0, 100_000), [0.0, -0.0, 709.78, -745.13, -708.4, -1e-300]])
+    y = orc.exp(x)
+    npy = np.exp(x)
+    normal = npy >= np.finfo(float).tiny
+    assert np.all(np.abs(y[normal] - npy[normal]) <= np.spacing(npy[normal]))
+    assert np.all(np.abs(y[~normal] - npy[~normal]) <= 5e-324)
+    ref = np.exp(x.astype(np.longdouble))
+    err = np.abs((y.astype(np.longdouble) - ref) / np.spacing(npy).astype(np.longdouble))
+    assert float(err[normal].max()) < 1.0
+    assert np.isnan(orc.exp(np.array([np.nan]))[0]) and orc.exp(np.array([800.0]))[0] == np.inf
+    assert orc.exp(np.array([-800.0]))[0] == 0.0
+
+
+def test_log_table_close_to_reference_pipeline(orc):
+    """build_table_log == build_table(exp(lw - max)) with the device exp; and
+    within the association drift of the reference's np.exp + build_weight_table."""
+    rng = np.random.default_rng(6)
+    for M in (1, 17, 8449, 300_000):
+        lw = -0.5 * rng.chisquare(6, size=M) + np.log(rng.dirichlet(np.ones(M))) if M > 1 else np.array([3.0])
+        W, st = orc.build_table_log(lw)
+        assert st == 0 and W[-1] == 1.0 and np.all(np.diff(W) >= 0)
+        Wd, _ = orc.build_table(orc.exp(lw - lw.max()))
+        np.testing.assert_array_equal(W, Wd)
+        Wp, _ = orc.port_build_table(np.exp(lw - lw.max()))
+        assert np.abs(W - Wp).max() <= 1e-12
+    _, st = orc.build_table_log(np.array([0.0, np.nan, 1.0]))
+    assert st & 0x1
