@@ -207,6 +207,24 @@ int dr_shard_match(const double *W, const double *idx, int64_t Mg, int64_t shard
                    const double *U, int64_t N, const int64_t *range, int64_t *out,
                    void *stream);
 
+/* Sharded sampling without replicating U.
+ * Step A on every rank: spacing tiles [t0, t1) of the n+1 spacings of the
+ * stream (k0, k1) at `offset` (rank g: t0 = nt g / G, t1 = nt (g+1) / G,
+ * nt = ceil((n+1) / (LANES*WARPS*K_UNIF))): agg[t1-t0] tile totals and
+ * zmin[t1-t0] spacing minima.  The caller all-gathers them. */
+int dr_shard_unif_totals(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, int64_t t0, int64_t t1,
+                         double *agg, double *zmin, void *stream);
+/* Step B: from all nt tile totals (agg_all) and nz spacing minima, fold the
+ * tile chain, regenerate only the tiles holding this rank's u's (those in
+ * (fl(O_g/T), fl(O_{g+1}/T)] of the table totals), repair collapses there
+ * and write U[i] for them (U is n long; other entries untouched);
+ * range4 = {i0, i1, first tile, last tile}, [i0, i1) the rank's slice.
+ * Bit-identical to dr_sorted_uniforms on the slice. */
+int dr_shard_unif_local(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, const double *agg_all,
+                        const double *zmin, int64_t nz, const double *totals, int32_t G, int32_t g,
+                        double *U, int64_t *range4, int32_t *status, void *ws, size_t ws_bytes,
+                        void *stream);
+
 /* --- either side of the path --- */
 
 /* The step after resampling: out[i][0..d) =

@@ -379,45 +379,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
     if (nsites || top) {
       if (t == 0 && threadIdx.x == 0) {
         // the forward / backward nextafter passes of randkit.py:104-116,
-        // restricted to the recorded collapse sites (see drs_scan.cu)
-        long long* sites = a.ws.sites;
-        double* U = a.U;
-        if (nsites > (uint32_t)SITE_CAP) {
-          double lo = 0.0;
-          for (int64_t i = 0; i < n; ++i) {
-            double v = ld_relaxed_f64(U + i);
-            if (v <= lo) { v = nextafter(lo, 1.0); U[i] = v; }
-            lo = v;
-          }
-        } else {
-          for (uint32_t q = 1; q < nsites; ++q) {
-            const long long key = sites[q];
-            int b = (int)q - 1;
-            while (b >= 0 && sites[b] > key) { sites[b + 1] = sites[b]; --b; }
-            sites[b + 1] = key;
-          }
-          int64_t done_to = -1;
-          for (uint32_t q = 0; q < nsites; ++q) {
-            int64_t i = sites[q];
-            if (i <= done_to) continue;
-            double lo = (i == 0) ? 0.0 : ld_relaxed_f64(U + i - 1);
-            while (i < n) {
-              const double v = ld_relaxed_f64(U + i);
-              if (!(v <= lo)) break;
-              lo = nextafter(lo, 1.0);
-              U[i] = lo;
-              ++i;
-            }
-            done_to = i;
-          }
-        }
-        double hi = 1.0;
-        for (int64_t i = n - 1; i >= 0; --i) {
-          const double v = ld_relaxed_f64(U + i);
-          if (!(v >= hi)) break;
-          hi = nextafter(hi, 0.0);
-          U[i] = hi;
-        }
+        // restricted to the recorded collapse sites
+        repair_sites(a.U, n, a.ws, nsites, true);
         s_flag = 1;
       }
       grid_barrier(bcount, bgen);

@@ -142,8 +142,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
   for (int64_t g = threadIdx.x; g < ng; g += CHAIN_THREADS) ws.grp[g] = sE[g];
 }
 
-static void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total,
-                         cudaStream_t st) {
+void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total,
+                  cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_chain_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
@@ -399,53 +399,6 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   }
 }
 
-__device__ void repair_sites(double* U, int64_t n, const ScanWS& ws, uint32_t nsites, bool top) {
-  // forward pass of randkit.py:107-111 restricted to the recorded collapse
-  // sites (every other position satisfies U[i] > lo and is left alone)
-  long long* sites = ws.sites;
-  if (nsites > (uint32_t)SITE_CAP) {
-    double lo = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
-      double v = ld_relaxed_f64(U + i);
-      if (v <= lo) { v = nextafter(lo, 1.0); U[i] = v; }
-      lo = v;
-    }
-  } else {
-    for (uint32_t a = 1; a < nsites; ++a) {  // insertion sort, nsites is tiny
-      const long long key = sites[a];
-      int b = (int)a - 1;
-      while (b >= 0 && sites[b] > key) { sites[b + 1] = sites[b]; --b; }
-      sites[b + 1] = key;
-    }
-    int64_t done_to = -1;
-    for (uint32_t a = 0; a < nsites; ++a) {
-      int64_t i = sites[a];
-      if (i <= done_to) continue;
-      double lo = (i == 0) ? 0.0 : ld_relaxed_f64(U + i - 1);
-      while (i < n) {
-        const double v = ld_relaxed_f64(U + i);
-        if (!(v <= lo)) break;
-        const double nv = nextafter(lo, 1.0);
-        U[i] = nv;
-        lo = nv;
-        ++i;
-      }
-      done_to = i;
-    }
-  }
-  // backward pass (randkit.py:112-116): stops at the first untouched entry,
-  // after which the forward-repaired prefix is strictly increasing below it
-  (void)top;
-  double hi = 1.0;
-  for (int64_t i = n - 1; i >= 0; --i) {
-    const double v = ld_relaxed_f64(U + i);
-    if (!(v >= hi)) break;
-    const double nv = nextafter(hi, 0.0);
-    U[i] = nv;
-    hi = nv;
-  }
-}
-
 // pass 2: U = Z / Z[n] in place (memory-bound: 16 bytes per u), collapse
 // sites recorded when the reference's exactness check fires (the repair and
 // the device stream advance follow in k_unif_finalize).
@@ -506,7 +459,7 @@ __global__ void k_unif_finalize(ScanWS ws, int64_t n, double* U, int32_t* status
   const uint32_t top = ws.hdr->top;
   int32_t st = 0;
   if (ws.hdr->need && (nsites > 0 || top)) {
-    repair_sites(U, n, ws, nsites, top != 0);
+    repair_sites(U, n, ws, nsites, true);  // the backward pass stops at the first untouched entry
     st |= DRS_ST_REPAIRED;
   }
   *status_out = st;

@@ -13,6 +13,9 @@ namespace drs {
 
 IndexDesc make_index_desc(int64_t M);
 int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st);
+void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total, cudaStream_t st);
+int64_t ws_capacity_tiles(size_t ws_bytes);
+ScanWS carve_ws(void* ws, size_t ws_bytes);
 
 __device__ __forceinline__ void fold_offsets(const double* totals, int G, int g, double& Og,
                                              double& Og1, double& T) {
@@ -81,6 +84,167 @@ __global__ void __launch_bounds__(256) k_shard_match(const double* __restrict__ 
     out[i] = shard_start + index_lower_bound(W, idx, d, __ldg(U + i));
 }
 
+// ---------------------------------------------- sharded sorted uniforms ----
+// Sampling over a W-sharded table without replicating U:
+//   1. rank g generates spacing tiles [t0, t1) (its 1/G of them): tile totals
+//      and spacing minima only (k_unif_tile_totals);
+//   2. the caller all-gathers them (one collective per call);
+//   3. every rank folds the identical tile chain, finds the tiles holding the
+//      u's of its W range (fl(O_g/T), fl(O_{g+1}/T)], regenerates just those
+//      tiles into U, repairs collapses there, and counts its slice
+//      (dr_shard_unif_local).  Values are bit-identical to dr_sorted_uniforms.
+constexpr int64_t TSU = (int64_t)THREADS * K_UNIF;
+
+__global__ void __launch_bounds__(THREADS) k_unif_tile_totals(PhiloxSpacings src, int64_t n, int64_t t0,
+                                                             double* __restrict__ agg, double* __restrict__ zmin) {
+  __shared__ FoldSmem fs;
+  __shared__ unsigned long long s_min;
+  __shared__ uint64_t s_words[PhiloxSpacings::SMEM_WORDS];
+  if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
+  const int64_t t = t0 + blockIdx.x;
+  const int64_t e0 = t * TSU + (int64_t)threadIdx.x * K_UNIF;
+  double z[K_UNIF];
+  src.tile(t, n + 1, src.position(), s_words, z);
+  unsigned long long mn = 0x7FF0000000000000ULL;
+#pragma unroll
+  for (int i = 0; i < K_UNIF; ++i)
+    if (e0 + i <= n) mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
+  double sc = z[0];
+#pragma unroll
+  for (int i = 1; i < K_UNIF; ++i) sc = __dadd_rn(sc, z[i]);
+  if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
+  double Q, R;
+  const double A = block_fold(sc, fs, Q, R);
+  if (threadIdx.x == 0) {
+    agg[blockIdx.x] = A;
+    zmin[blockIdx.x] = __longlong_as_double((long long)s_min);
+  }
+}
+
+__global__ void k_stage_chain(const double* __restrict__ agg_all, const double* __restrict__ zmin, int64_t nz,
+                              int64_t nt, ScanWS ws) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += stride) {
+    ws.agg[t] = agg_all[t];
+    ws.incl[t] = (t < nz) ? zmin[t] : __longlong_as_double(0x7FF0000000000000LL);
+  }
+}
+
+// u at the last element of tile t: S = C + (D + A) (the tile's inclusive prefix)
+__device__ __forceinline__ double tile_end_u(const ScanWS& ws, int64_t t, double total) {
+  return __ddiv_rn(__dadd_rn(ws.grp[t / GROUP_TILES], __dadd_rn(ws.incl[t], ws.agg[t])), total);
+}
+
+__global__ void k_unif_tile_range(ScanWS ws, int64_t nt, const double* __restrict__ totals, int G, int g,
+                                  int64_t* rng, double* U) {
+  double Og, Og1, T;
+  fold_offsets(totals, G, g, Og, Og1, T);
+  const double lo = fmin(__ddiv_rn(Og, T), 1.0), hi = fmin(__ddiv_rn(Og1, T), 1.0);
+  const double total = ws.hdr->total;
+  // tiles 0 .. nt-2 end on a u (the last tile holds the final spacing)
+  int64_t a = 0, b = nt - 1;  // first t in [0, nt-1) with u_end(t) > lo, else nt-1
+  if (g > 0)
+    while (a < b) {
+      const int64_t m = (a + b) / 2;
+      if (tile_end_u(ws, m, total) > lo) b = m;
+      else a = m + 1;
+    }
+  int64_t c = (g < G - 1) ? 0 : nt - 1, d = nt - 1;  // first t in [0, nt-1) with u_end(t) >= hi, else nt-1
+  if (g < G - 1)
+    while (c < d) {
+      const int64_t m = (c + d) / 2;
+      if (tile_end_u(ws, m, total) >= hi) d = m;
+      else c = m + 1;
+    }
+  rng[2] = a;
+  rng[3] = c > a ? c : a;
+  // the u just before the range (the previous tile's inclusive prefix): the
+  // repair's forward pass reads it when the first u of the range collapses
+  if (a > 0) U[a * TSU - 1] = tile_end_u(ws, a - 1, total);
+}
+
+__global__ void __launch_bounds__(THREADS) k_unif_pass_range(PhiloxSpacings src, int64_t n, ScanWS ws,
+                                                            const int64_t* __restrict__ rng,
+                                                            double* __restrict__ U) {
+  __shared__ FoldSmem fs;
+  __shared__ double s_last[WARPS];
+  __shared__ uint64_t s_words[PhiloxSpacings::SMEM_WORDS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double total = ws.hdr->total;
+  const bool need = ws.hdr->need != 0u;
+  // grid-stride over this rank's tiles [rng[2], rng[3]] (read on the device:
+  // no host round trip, no idle CTAs for the other ranks' tiles)
+  for (int64_t t = rng[2] + blockIdx.x; t <= rng[3]; t += gridDim.x) {
+    const int64_t e0 = t * TSU + (int64_t)threadIdx.x * K_UNIF;
+    double z[K_UNIF];
+    src.tile(t, n + 1, src.position(), s_words, z);
+    double sc[K_UNIF];
+    sc[0] = z[0];
+#pragma unroll
+    for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+    double Q, R;
+    block_fold(sc[K_UNIF - 1], fs, Q, R);
+    const double C = ws.grp[t / GROUP_TILES], D = ws.incl[t];
+    double u[K_UNIF];
+#pragma unroll
+    for (int i = 0; i < K_UNIF; ++i) {
+      u[i] = __ddiv_rn(__dadd_rn(C, __dadd_rn(D, __dadd_rn(R, __dadd_rn(Q, sc[i])))), total);
+      if (e0 + i < n) U[e0 + i] = u[i];
+    }
+    if (need) {  // collapse sites, exactly as k_unif_pass2
+      double prev_lane = __shfl_up_sync(FULL, u[K_UNIF - 1], 1);
+      if (lane == 31) s_last[warp] = u[K_UNIF - 1];
+      __syncthreads();
+      if (lane == 0)
+        prev_lane = (warp > 0) ? s_last[warp - 1] : ((t == 0) ? 0.0 : __ddiv_rn(__dadd_rn(C, D), total));
+#pragma unroll
+      for (int i = 0; i < K_UNIF; ++i) {
+        const int64_t e = e0 + i;
+        if (e < n) {
+          const double pv = (i == 0) ? prev_lane : u[i - 1];
+          if (u[i] <= pv) {
+            const uint32_t slot = atomicAdd(&ws.hdr->nsites, 1u);
+            if (slot < (uint32_t)SITE_CAP) ws.sites[slot] = (long long)e;
+          }
+          if (e == n - 1 && u[i] >= 1.0) atomicOr(&ws.hdr->top, 1u);
+        }
+      }
+    }
+    __syncthreads();  // fs / s_last reuse by the next tile
+  }
+}
+
+// repair inside the range (the backward pass only on the rank holding the
+// last tile), the slice counts, status, counters back to zero
+__global__ void k_unif_local_finish(ScanWS ws, int64_t n, int64_t nt, double* U, const double* __restrict__ totals,
+                                    int G, int g, int64_t* rng, int32_t* status) {
+  const int64_t ta = rng[2], tb = rng[3];
+  const int64_t base = ta * TSU, end = min((tb + 1) * TSU, n);
+  if (threadIdx.x == 0) {
+    const uint32_t nsites = ws.hdr->nsites;
+    const uint32_t top = ws.hdr->top;
+    int32_t st = 0;
+    if (ws.hdr->need && (nsites > 0 || top)) {
+      repair_sites(U, end, ws, nsites, tb == nt - 1, base);
+      st |= DRS_ST_REPAIRED;
+    }
+    *status = st;
+    ws.hdr->nsites = 0;
+    ws.hdr->top = 0;
+  }
+  __syncthreads();
+  double Og, Og1, T;
+  fold_offsets(totals, G, g, Og, Og1, T);
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    const int64_t v = (g == 0) ? 0 : base + warp_count_le_s(U + base, end - base, fmin(__ddiv_rn(Og, T), 1.0));
+    if ((threadIdx.x & 31) == 0) rng[0] = v;
+  } else if (warp == 1) {
+    const int64_t v = (g == G - 1) ? n : base + warp_count_le_s(U + base, end - base, fmin(__ddiv_rn(Og1, T), 1.0));
+    if ((threadIdx.x & 31) == 0) rng[1] = v;
+  }
+}
+
 }  // namespace drs
 
 using namespace drs;
@@ -113,6 +277,36 @@ int dr_shard_match(const double* W, const double* idx, int64_t Mg, int64_t shard
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
   const int64_t blocks = cdiv(N, 256) < 148 * 16 ? cdiv(N, 256) : 148 * 16;
   k_shard_match<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(W, idx, d, shard_start, U, range, out);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
+int dr_shard_unif_totals(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, int64_t t0, int64_t t1,
+                         double* agg, double* zmin, void* stream) {
+  if (n < 1 || t0 < 0 || t1 < t0 || !agg || !zmin) return DRS_ERR_ARG;
+  if (t1 > cdiv(n + 1, TSU)) return DRS_ERR_ARG;
+  if (t1 == t0) return DRS_OK;
+  PhiloxSpacings src{k0, k1, offset, nullptr};
+  k_unif_tile_totals<<<(unsigned)(t1 - t0), THREADS, 0, (cudaStream_t)stream>>>(src, n, t0, agg, zmin);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
+int dr_shard_unif_local(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, const double* agg_all,
+                        const double* zmin, int64_t nz, const double* totals, int32_t G, int32_t g, double* U,
+                        int64_t* range4, int32_t* status, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 1 || !agg_all || !zmin || nz < 1 || !totals || G < 1 || g < 0 || g >= G || !U || !range4 || !status ||
+      !ws)
+    return DRS_ERR_ARG;
+  const int64_t nt = cdiv(n + 1, TSU);
+  if (nt > ws_capacity_tiles(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)4096 * GROUP_TILES) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const ScanWS s = carve_ws(ws, ws_bytes);
+  PhiloxSpacings src{k0, k1, offset, nullptr};
+  k_stage_chain<<<(unsigned)(cdiv(nt, 256) < 1184 ? cdiv(nt, 256) : 1184), 256, 0, st>>>(agg_all, zmin, nz, nt, s);
+  launch_chain(s, nt, 1, nullptr, nullptr, st);
+  k_unif_tile_range<<<1, 1, 0, st>>>(s, nt, totals, G, g, range4, U);
+  k_unif_pass_range<<<(unsigned)(nt < 148 * 4 ? nt : 148 * 4), THREADS, 0, st>>>(src, n, s, range4, U);
+  k_unif_local_finish<<<1, 64, 0, st>>>(s, n, nt, U, totals, G, g, range4, status);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 

@@ -9,9 +9,13 @@ The multi-GPU mode of the north star (config 5, M = 2^30): rank g of G owns
 3. ``dr_shard_finalize``: O_g = T_0 + ... + T_{g-1} and T = O_G folded in
    rank order on every rank, W = min((O_g + S)/T, 1) in place, index built.
    Rank g's lower boundary fl(O_g/T) is bit-identical to rank g-1's last W.
-4. Sampling: every rank regenerates the same sorted U (same stream), finds
-   its slice (fl(O_g/T), fl(O_{g+1}/T)] on the device and matches only that
-   slice against its shard -- no further communication.
+4. Sampling without replicating U: rank g generates the totals of its 1/G of
+   the spacing tiles (``dr_shard_unif_totals``); ONE all-gather of those
+   totals (8 bytes per tile, plus the tiles' spacing minima); every rank folds
+   the identical tile chain, regenerates only the tiles holding the u's of its
+   W range (fl(O_g/T), fl(O_{g+1}/T)] and matches that slice against its
+   shard (``dr_shard_unif_local``, ``dr_shard_match``).  The U values are
+   bit-identical to ``dr_sorted_uniforms`` on every slice.
 
 The compute steps go through an ``ops`` object (default: the CUDA library)
 so that the collective logic can be exercised on CPU ranks with gloo in the
@@ -59,17 +63,34 @@ class DeviceShardOps:
                         "dr_shard_finalize")
         return S, idx
 
-    def sorted_uniforms(self, stream, n: int) -> torch.Tensor:
-        from .randkit import sorted_uniforms_device
+    def tile_size(self) -> int:
+        lanes, warps, _, k_unif, _, _ = self._lib.scan_geometry()
+        return lanes * warps * k_unif
 
-        return sorted_uniforms_device(stream, n)
+    def unif_tile_totals(self, key, offset: int, n: int, t0: int, t1: int):
+        dev = self.device()
+        agg = torch.empty(max(t1 - t0, 1), dtype=torch.float64, device=dev)
+        zmin = torch.empty(max(t1 - t0, 1), dtype=torch.float64, device=dev)
+        self._lib.check(self._lib.lib().dr_shard_unif_totals(key[0], key[1], offset, n, t0, t1, agg.data_ptr(),
+                                                             zmin.data_ptr(), self._lib.stream_handle()),
+                        "dr_shard_unif_totals")
+        return agg[: t1 - t0], zmin[: t1 - t0]
 
-    def shard_range(self, U: torch.Tensor, totals: torch.Tensor, G: int, g: int) -> torch.Tensor:
-        rng = torch.empty(2, dtype=torch.int64, device=U.device)
-        self._lib.check(self._lib.lib().dr_shard_range(U.data_ptr(), U.numel(), totals.data_ptr(), G, g,
-                                                       rng.data_ptr(), self._lib.stream_handle()),
-                        "dr_shard_range")
-        return rng
+    def unif_local(self, key, offset: int, n: int, agg_all: torch.Tensor, zmin_all: torch.Tensor,
+                   totals: torch.Tensor, G: int, g: int):
+        L = self._lib.lib()
+        dev = self.device()
+        U = torch.empty(n, dtype=torch.float64, device=dev)
+        rng = torch.zeros(4, dtype=torch.int64, device=dev)
+        st = torch.zeros(1, dtype=torch.int32, device=dev)
+        ws, wsb = self._lib.workspace(self._lib.workspace_bytes(self._lib.OP_SORTED, n))
+        agg_all = agg_all.contiguous()
+        zmin_all = zmin_all.contiguous()
+        self._lib.check(L.dr_shard_unif_local(key[0], key[1], offset, n, agg_all.data_ptr(), zmin_all.data_ptr(),
+                                              zmin_all.numel(), totals.data_ptr(), G, g, U.data_ptr(),
+                                              rng.data_ptr(), st.data_ptr(), ws, wsb, self._lib.stream_handle()),
+                        "dr_shard_unif_local")
+        return U, rng
 
     def shard_match(self, table: "ShardedWeightTable", U: torch.Tensor, rng: torch.Tensor) -> torch.Tensor:
         out = torch.full((U.numel(),), -1, dtype=torch.int64, device=U.device)
@@ -149,18 +170,48 @@ def build_sharded_table(raw_shard, *, group=None, ops=None) -> ShardedWeightTabl
     return ShardedWeightTable(W=W, index=idx, totals=totals, sizes=sizes, rank=g, world=G, group=group)
 
 
+def _key_and_take(stream, k: int):
+    """(Philox key, draw offset) of the next k draws; advances the stream."""
+    if hasattr(stream, "_take"):
+        return stream.key, stream._take(k)
+    off = stream.position
+    stream.position += k
+    return stream.key, off
+
+
 def sharded_dac_sampler(table: ShardedWeightTable, n: int, stream, *, ops=None, gather: bool = False):
     """dac_sampler over a sharded table (samplers.py:262-266 semantics).
 
-    Every rank draws the same sorted U from ``stream`` (which must be
-    identical on all ranks) and fills the entries of its own slice.  Returns
-    ``(out, range)``: ``out`` int64[n] with this rank's slice filled (-1
-    elsewhere) and ``range`` = (i0, i1) on the device.  ``gather=True``
-    all-reduces (max) so every rank holds the full index array.
+    ``stream`` must be identical on all ranks.  Rank g generates the totals
+    of its 1/G of the spacing tiles; one all-gather of those totals; then
+    each rank regenerates only the tiles holding its u's and matches them
+    against its shard.  Returns ``(out, range)``: ``out`` int64[n] with this
+    rank's slice filled (-1 elsewhere) and ``range`` = (i0, i1, first tile,
+    last tile) on the device.  ``gather=True`` all-reduces (max) so every
+    rank holds the full index array.
     """
     ops = ops or DeviceShardOps()
-    U = ops.sorted_uniforms(stream, int(n))
-    rng = ops.shard_range(U, table.totals, table.world, table.rank)
+    n = int(n)
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    G, g = table.world, table.rank
+    ts = ops.tile_size()
+    nt = (n + 1 + ts - 1) // ts
+    bounds = [nt * h // G for h in range(G + 1)]
+    t0, t1 = bounds[g], bounds[g + 1]
+    width = (nt + G - 1) // G
+    key, off = _key_and_take(stream, n + 1)
+    agg, zmin = ops.unif_tile_totals(key, off, n, t0, t1)
+    mine = torch.zeros(2 * width, dtype=torch.float64, device=agg.device)
+    mine[width:] = float("inf")
+    mine[: t1 - t0] = agg
+    mine[width: width + t1 - t0] = zmin
+    allv = torch.empty(G * 2 * width, dtype=torch.float64, device=agg.device)
+    dist.all_gather_into_tensor(allv, mine, group=table.group)
+    allv = allv.reshape(G, 2 * width)
+    agg_all = torch.cat([allv[h, : bounds[h + 1] - bounds[h]] for h in range(G)])
+    zmin_all = torch.cat([allv[h, width: width + bounds[h + 1] - bounds[h]] for h in range(G)])
+    U, rng = ops.unif_local(key, off, n, agg_all, zmin_all, table.totals, G, g)
     out = ops.shard_match(table, U, rng)
     if gather:
         dist.all_reduce(out, op=dist.ReduceOp.MAX, group=table.group)

@@ -341,36 +341,48 @@ def test_batched_invalid_weights_raise(drs):
 
 
 def test_sharded_single_gpu_emulation(drs, orc):
-    """The shard steps for G shards run one after another on one GPU, with the
-    all-gather replaced by stacking the totals; result == oracle sharded table."""
+    """The shard steps for G ranks run one after another on one GPU, with the
+    all-gathers replaced by concatenation: the sharded table == the oracle's,
+    every rank's U slice == dr_sorted_uniforms bit for bit although each rank
+    generated only its 1/G of the spacing tiles, the slices tile [0, N), and
+    the indices == the oracle's DaC on the whole table."""
     from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable
 
     ops = DeviceShardOps()
     rng = np.random.default_rng(1005)
-    M, N = 1 << 20, 1 << 14
+    M, N = 1 << 20, (1 << 17) + 3
     w = np.exp(2 * rng.standard_normal(M))
     off = rng.integers(0, M - 1024)
     w[off:off + 1024] = (w.sum() - w[off:off + 1024].sum()) / 3 / 1024
-    for G in (1, 2, 4):
+    k0, k1 = orc.key_of(2005)
+    Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+    ts = ops.tile_size()
+    nt = (N + 1 + ts - 1) // ts
+    for G in (1, 2, 4, 8):
         parts = [dev(w[M * g // G: M * (g + 1) // G]) for g in range(G)]
         scans = [ops.shard_scan(p) for p in parts]
         totals = torch.cat([s[1] for s in scans])
         Wo, To, st = orc.build_table_sharded(w, G)
         np.testing.assert_array_equal(totals.cpu().numpy(), To)
+        bounds = [nt * h // G for h in range(G + 1)]
+        shares = [ops.unif_tile_totals((k0, k1), 0, N, bounds[h], bounds[h + 1]) for h in range(G)]
+        agg_all = torch.cat([a for a, _ in shares])
+        zmin_all = torch.cat([z for _, z in shares])
         full = torch.full((N,), -1, dtype=torch.int64, device="cuda")
-        Ws = []
+        Ws, prev = [], 0
         for g in range(G):
             W, idx = ops.finalize(scans[g][0], totals, G, g)
             Ws.append(W.cpu().numpy())
             tab = ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g, world=G)
-            U = ops.sorted_uniforms(drs.RngStream(2005), N)
-            rngd = ops.shard_range(U, totals, G, g)
+            U, rngd = ops.unif_local((k0, k1), 0, N, agg_all, zmin_all, totals, G, g)
+            a, b, ta, tb = rngd.tolist()
+            assert a == prev and ta * ts <= a and b <= min((tb + 1) * ts, N)
+            prev = b
+            np.testing.assert_array_equal(U[a:b].cpu().numpy(), Uo[a:b])
             o = ops.shard_match(tab, U, rngd)
-            a, b = rngd.tolist()
             full[a:b] = o[a:b]
+        assert prev == N
         np.testing.assert_array_equal(np.concatenate(Ws), Wo)
-        k0, k1 = orc.key_of(2005)
-        Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
         np.testing.assert_array_equal(full.cpu().numpy(), orc.match("dac", Wo, Uo))
 
 

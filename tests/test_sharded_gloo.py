@@ -66,22 +66,40 @@ class OracleShardOps:
             W[-1] = 1.0
         return torch.from_numpy(W), torch.from_numpy(self.orc.build_index(W))
 
-    def sorted_uniforms(self, stream, n):
-        U, _ = self.orc.sorted_uniforms(stream.key[0], stream.key[1], stream.position, n)
-        stream.position += n + 1
-        return torch.from_numpy(U)
+    def tile_size(self):
+        return 32 * 8 * 2  # LANES * WARPS * K_UNIF of the device association
 
-    def shard_range(self, U, totals, G, g):
+    def _spacings(self, key, offset, n):
+        return self.orc.neglog(self.orc.uniforms(key[0], key[1], offset, n + 1))
+
+    def unif_tile_totals(self, key, offset, n, t0, t1):
+        ts = self.tile_size()
+        z = self._spacings(key, offset, n)
+        agg, zmin = [], []
+        for t in range(t0, t1):
+            zt = np.zeros(ts)
+            part = z[t * ts:(t + 1) * ts]
+            zt[: part.size] = part
+            agg.append(self.orc.chain_scan(zt, 2)[1])
+            zmin.append(part.min())
+        return torch.tensor(agg, dtype=torch.float64), torch.tensor(zmin, dtype=torch.float64)
+
+    def unif_local(self, key, offset, n, agg_all, zmin_all, totals, G, g):
+        ts = self.tile_size()
+        # the gathered tile totals are exactly this stream's (all ranks' shares)
+        nt = (n + 1 + ts - 1) // ts
+        ref, _ = self.unif_tile_totals(key, offset, n, 0, nt)
+        assert np.array_equal(agg_all.numpy(), ref.numpy())
+        U, _ = self.orc.sorted_uniforms(key[0], key[1], offset, n)
         tv = totals.tolist()
         T = self._fold(tv, G)
-        u = U.numpy()
-        lo = 0 if g == 0 else int(np.searchsorted(u, min(self._fold(tv, g) / T, 1.0), side="right"))
-        hi = u.shape[0] if g == G - 1 else int(np.searchsorted(u, min(self._fold(tv, g + 1) / T, 1.0), side="right"))
-        return torch.tensor([lo, hi], dtype=torch.int64)
+        lo = 0 if g == 0 else int(np.searchsorted(U, min(self._fold(tv, g) / T, 1.0), side="right"))
+        hi = n if g == G - 1 else int(np.searchsorted(U, min(self._fold(tv, g + 1) / T, 1.0), side="right"))
+        return torch.from_numpy(U), torch.tensor([lo, hi, 0, nt - 1], dtype=torch.int64)
 
     def shard_match(self, table, U, rng):
         out = torch.full((U.numel(),), -1, dtype=torch.int64)
-        a, b = rng.tolist()
+        a, b = rng.tolist()[:2]
         W = table.W.numpy()
         u = U.numpy()
         for i in range(a, b):
@@ -157,6 +175,7 @@ def test_sharded_table_and_sampler_match_oracle(orc, world):
     assert ranges[0][0] == 0 and ranges[-1][1] == N
     for r0, r1 in zip(ranges, ranges[1:]):
         assert r0[1] == r1[0]
+    assert [r[1] for r in res] == ["ok"] * world
     for r in res:  # gather=True: every rank holds the full index array
         np.testing.assert_array_equal(r[2][2], expect)
 
