@@ -6,8 +6,10 @@ M = 2^26 heavy-tailed weights (log w ~ N(0, 4^2), seed 1003), N = 2^16 draws
 (stream seed 2003).  A step is one sampler call: sorted uniforms + search,
 with the table already built and resident (the reference's timed region,
 bench.py:193-204).  Metric = algorithmic bytes (8M + 16N) / step time, plus
-samples/s.  L2 is flushed (256 MiB write) before every timed step; steps
-are timed one by one with CUDA events on the launching stream.
+samples/s.  A step is one public-API call (device-resident result); L2 is
+flushed (256 MiB write) before every timed step; steps are timed one by one
+with CUDA events on the launching stream.  The same call replayed from a
+CUDA graph (stream position on the device) is reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5]
                   [--sampler dac|ccf|binary] [--mode auto|merge|search]
@@ -207,12 +209,13 @@ def run_drs(args, rank, world, local_rank):
             return sampler(table, N, stream, device=True, out=out_buf, **kw)
 
         step = eager_step
+        graph_step = None
         fused = args.sampler == "dac" and args.mode != "merge" and M > 16 * N and (N + 1) <= 148 * 512
         # sorted uniforms = pass 1 + chain + pass 2 + finalize, then the search
         launches_per_step = {"binary": 1, "ccf": 5}.get(args.sampler, 1 if fused else 5)
         if args.graph:
-            # one sampler call captured once; the stream position lives on the
-            # device, so every replay draws fresh uniforms
+            # the same call captured once in a CUDA graph; the stream position
+            # lives on the device, so every replay draws fresh uniforms
             dstream = drs.DeviceRngStream(c["useed"], (rank,))
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream())
@@ -222,17 +225,17 @@ def run_drs(args, rank, world, local_rank):
                 with torch.cuda.graph(graph, stream=side):
                     sampler(table, N, dstream, device=True, out=out_buf, **kw)
             torch.cuda.current_stream().wait_stream(side)
-            if args.sampler == "binary":
-                launches_per_step += 1  # the device-side stream advance
 
-            def step():
+            def graph_step():
                 graph.replay()
         # the dominant kernel alone: the search over a fixed U
         U = drs.randkit.sorted_uniforms_device(drs.RngStream(c["useed"], (rank, 7)), N)
         match = {"dac": lambda: drs.dac_match(U, table, check=False, mode=args.mode),
                  "ccf": lambda: drs.ccf_match(U, table, check=False),
                  "binary": lambda: drs.samplers._lower_bounds(table, U)}[args.sampler]
-        kernel_step = match
+        # the dominant kernel: the fused sampler kernel when the step is that one
+        # launch, else the search over a fixed U
+        kernel_step = eager_step if (fused and args.sampler == "dac") else match
         e2e_step = lambda: sampler(table, N, stream, **kw)  # noqa: E731
         e2e_h2d, e2e_d2h = 0, 8 * N
 
@@ -258,11 +261,16 @@ def run_drs(args, rank, world, local_rank):
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clk:
+        time.sleep(0.2)  # the first nvidia-smi sample is taken before the timed steps start
+        step()
+        torch.cuda.synchronize()
         step_ms = timed(step, args.steps)
     barrier()
-    eager_ms = None
-    if step is not locals().get("eager_step", step):
-        eager_ms = statistics.median(timed(eager_step, args.steps))
+    graph_ms = None
+    if cfg not in ("c4",) and not (cfg == "c5" and world > 1) and locals().get("graph_step") is not None:
+        for _ in range(3):
+            graph_step()
+        graph_ms = statistics.median(timed(graph_step, args.steps))
     total_ms = float(sum(step_ms))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -355,9 +363,9 @@ def run_drs(args, rank, world, local_rank):
         "table_build": table_build,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
-        "timing": "CUDA-graph replay of one sampler call (device-resident stream position)"
-                  if eager_ms is not None else "eager public-API calls",
-        "eager_ms_per_step_median": eager_ms,
+        "timing": "one public-API sampler call per step (device result), CUDA events on the launching stream",
+        "steps_ms": [round(x, 5) for x in step_ms],
+        "graph_replay_ms_per_step_median": graph_ms,
     }
     return line, (alg_bytes, samples)
 

@@ -31,7 +31,7 @@ extern "C" {
 #define DRS_SCAN_WARPS 8
 #define DRS_SCAN_K_TABLE 33 /* elements per lane chunk, table scans   */
 #define DRS_SCAN_K_UNIF 2   /* elements per lane chunk, spacing scans */
-#define DRS_SCAN_GROUP 256  /* tiles per group of the tile chain          */
+#define DRS_SCAN_GROUP 32   /* tiles per group of the tile chain          */
 #define DRS_INDEX_FANOUT 16
 #define DRS_INDEX_MAX_LEVELS 12
 

@@ -39,7 +39,7 @@ extern "C" {
 #define DRS_REF_K_TABLE 33
 #define DRS_REF_K_UNIF 2
 #define DRS_REF_FANOUT 16
-#define DRS_REF_GROUP 256 /* tiles per group of the tile chain */
+#define DRS_REF_GROUP 32 /* tiles per group of the tile chain */
 
 /* status bits (same values as include/drs.h) */
 #define DRS_REF_ST_INVALID_WEIGHT 0x1

@@ -38,11 +38,14 @@ int launch_index(const double* W, const double* idx, int64_t M, const double* u,
                  int64_t* out, cudaStream_t st);
 
 constexpr int SIDX_CAP = 24576;
-constexpr int FUSED_MAX_TILES = 160;   // >= co-resident CTAs (148 SMs x 1); <= FLAG_CAP
+constexpr int FUSED_MAX_TILES = 1024;  // 32 lanes x GROUP_TILES; the launch also needs co-residency
 #ifndef DRS_L2_PREFETCH_MB
-#define DRS_L2_PREFETCH_MB 48
+#define DRS_L2_PREFETCH_MB 4
 #endif
-constexpr int64_t L2_PREFETCH_DOUBLES = (int64_t)DRS_L2_PREFETCH_MB << 17;  // MB of global index levels  // doubles of index kept in shared memory (192 KB, 1 CTA per SM)
+// the first global index level below the shared-memory levels (2 MB at
+// M = 2^26) is prefetched into L2 while the uniforms are formed; the larger
+// levels and W are reached at random and are left to the searches
+constexpr int64_t L2_PREFETCH_DOUBLES = (int64_t)DRS_L2_PREFETCH_MB << 17;
 constexpr int64_t TS_U = (int64_t)THREADS * K_UNIF;
 
 struct SmemLevels {
@@ -215,9 +218,15 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   // not queue behind these bulk transfers
   if (threadIdx.x == THREADS - 32) {
     mbar_init(&bar, 1);
+#if defined(DRS_EXP_NO_STAGE)
+    mbar_expect_tx(&bar, 0);  // experiment: no index staging
+#else
     mbar_expect_tx(&bar, sbytes);
     if (sbytes) bulk_g2s(sidx, a.idx + a.sl.base, sbytes, &bar);
-    const int64_t plo = a.sl.base > L2_PREFETCH_DOUBLES ? a.sl.base - L2_PREFETCH_DOUBLES : 0;
+#endif
+    const int64_t lvl = (a.sl.k_smem >= 2) ? a.sl.base - a.d.off[a.sl.k_smem - 1] : 0;  // doubles
+    const int64_t cap = lvl < L2_PREFETCH_DOUBLES ? lvl : L2_PREFETCH_DOUBLES;
+    const int64_t plo = a.sl.base - cap;
     const int64_t per = cdiv(cdiv(a.sl.base - plo, (int64_t)gridDim.x), 2) * 2;  // 16-byte multiples
     const int64_t p0 = plo + t * per, p1 = min(a.sl.base, p0 + per) & ~(int64_t)1;
     for (int64_t p = p0 & ~(int64_t)1; p < p1; p += 8192)  // 64 KB pieces
@@ -252,89 +261,74 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   const double A = block_fold(sc[K_UNIF - 1], fs, Q, R);
   STAMP(2);
   STAMP(3);
+  // 3. the tile chain: every CTA publishes its total and spacing minimum and
+  // bumps the arrival counter of this call's parity (cnt[gen & 1]); thread 0
+  // of every CTA polls that one word until all nt tiles arrived, then warp 0
+  // loads the nt totals (one coalesced round trip) and folds the chain in
+  // tile order itself (D inside groups of GROUP_TILES tiles, C over the
+  // groups).  CTA 0 zeroes the other parity's counter for the next call and
+  // advances the generation; no grid barrier, no leader hop.
+  unsigned long long* cnt = a.ws.tflag + FLAG_CAP - 2;  // two 64-bit counters, by parity
   if (threadIdx.x == 0) {
     st_relaxed_f64(&a.ws.agg[t], A);
     st_relaxed_f64(&a.ws.incl[t], __longlong_as_double((long long)s_min));
-    st_release_u64(&a.ws.tflag[t], gen + 1);  // tile t published for this call
+    __threadfence();
+    atomicAdd(cnt + (gen & 1), 1ull);
+    while (ld_acquire_u64(cnt + (gen & 1)) < (unsigned long long)nt) __nanosleep(64);
   }
-
-  // 3. the tile chain, folded once: CTA 0 waits for every tile's flag (at
-  // generation gen + 1), folds the totals in tile order (D inside groups of
-  // GROUP_TILES tiles, C over the groups), writes each tile's (C, D), the
-  // total and the spacing minimum, then releases hdr->fgen = gen + 1; every
-  // other CTA polls that single word (one poller per CTA, no all-to-all).
-  if (t == 0 && warp == 0) {
-    double va[FUSED_MAX_TILES / 32], vm[FUSED_MAX_TILES / 32];
-    double vc[FUSED_MAX_TILES / 32], vd[FUSED_MAX_TILES / 32];
-    while (true) {  // poll all flags together (independent loads)
-      bool ok = true;
-#pragma unroll
-      for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
-        const int64_t tt = q * 32 + lane;
-        if (tt < nt) ok &= (ld_acquire_u64(&a.ws.tflag[tt]) == gen + 1);
-      }
-      if (__all_sync(FULL, ok)) break;
-      __nanosleep(20);
-    }
-#pragma unroll
-    for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
-      const int64_t tt = q * 32 + lane;
-      va[q] = (tt < nt) ? ld_relaxed_f64(&a.ws.agg[tt]) : 0.0;
-      vm[q] = (tt < nt) ? ld_relaxed_f64(&a.ws.incl[tt]) : __longlong_as_double(0x7FF0000000000000LL);
-      vc[q] = 0.0;
-      vd[q] = 0.0;
-    }
-    double C = 0.0, D = 0.0;
+  __syncthreads();
+  STAMP(9);
+  if (warp == 0) {
+    // lane g folds group g (tiles 32g .. 32g+31) serially; lane 0 then folds
+    // the group totals: a 32 + ng step chain instead of nt steps
+    static_assert(GROUP_TILES == 32, "one lane per group of 32 tiles");
     unsigned long long gmin = 0x7FF0000000000000ULL;
+    double D = 0.0, Dt = 0.0;
+    const int64_t gb = (int64_t)lane * GROUP_TILES;
+    if (threadIdx.x == 0) STAMP1(10);
+    if (gb < nt) {
+      double v[GROUP_TILES];
+      // L2 loads (.cg: no stale L1 copies of the previous call's values), all
+      // issued before the first use
+      double m[GROUP_TILES];
 #pragma unroll
-    for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
-      const int64_t base = q * 32;
-      if (base >= nt) break;
-      gmin = min(gmin, (unsigned long long)__double_as_longlong(vm[q]));
-      // fully unrolled: the 32 shuffles issue back to back and only the adds
-      // chain; tiles past nt contribute +0.0, which leaves the fold unchanged
-      double vk[32];
-#pragma unroll
-      for (int k = 0; k < 32; ++k) vk[k] = __shfl_sync(FULL, va[q], k);
-      if (base > 0 && base % GROUP_TILES == 0) {  // group boundary (32 | GROUP_TILES)
-        C = __dadd_rn(C, D);
-        D = 0.0;
+      for (int k = 0; k < GROUP_TILES; ++k) {
+        v[k] = (gb + k < nt) ? __ldcg(&a.ws.agg[gb + k]) : 0.0;
+        m[k] = (gb + k < nt) ? __ldcg(&a.ws.incl[gb + k]) : __longlong_as_double(0x7FF0000000000000LL);
       }
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        vc[q] = (lane == k) ? C : vc[q];
-        vd[q] = (lane == k) ? D : vd[q];
-        D = __dadd_rn(D, vk[k]);
-      }
-    }
-    const double total = __dadd_rn(C, D);
-    for (int o = 16; o > 0; o >>= 1) gmin = min(gmin, __shfl_xor_sync(FULL, gmin, o));
+      for (int k = 0; k < GROUP_TILES; ++k) gmin = min(gmin, (unsigned long long)__double_as_longlong(m[k]));
+      if (threadIdx.x == 0) STAMP1(11);
 #pragma unroll
-    for (int q = 0; q < FUSED_MAX_TILES / 32; ++q) {
-      const int64_t tt = q * 32 + lane;
-      if (tt < nt) {
-        st_relaxed_f64(&a.ws.agg[tt], vd[q]);
-        st_relaxed_f64(&a.ws.incl[tt], vc[q]);
+      for (int k = 0; k < GROUP_TILES; ++k) {
+        Dt = (gb + k == t) ? D : Dt;
+        D = __dadd_rn(D, v[k]);  // tiles past nt add +0.0: the fold is unchanged
       }
     }
-    if (lane == 0) {
-      s_C = vc[0];
-      s_P = vd[0];
-      s_total = total;
-      s_min = gmin;
-      a.ws.hdr->total = total;
-      a.ws.hdr->zmin_bits = gmin;
+    if (t == 0 && lane == 0) {
       // every CTA has read the stream position and the generation
       if (a.offset_dev) *a.offset_dev = offset + (uint64_t)(n + 1);
+      cnt[(gen + 1) & 1] = 0ull;  // the next call's counter
+      a.ws.hdr->fgen = gen + 1;
     }
-    __syncwarp();
-    if (lane == 0) st_release_u64(&a.ws.hdr->fgen, gen + 1);
-  } else if (t != 0 && threadIdx.x == 0) {
-    while (ld_acquire_u64(&a.ws.hdr->fgen) != gen + 1) __nanosleep(64);
-    s_C = ld_relaxed_f64(&a.ws.incl[t]);
-    s_P = ld_relaxed_f64(&a.ws.agg[t]);
-    s_total = ld_relaxed_f64(&a.ws.hdr->total);
-    s_min = *(volatile unsigned long long*)&a.ws.hdr->zmin_bits;
+    if (threadIdx.x == 0) STAMP1(12);
+    const int ng = (int)cdiv(nt, GROUP_TILES);
+    double C = 0.0, Ct = 0.0;
+    for (int g = 0; g < ng; ++g) {  // C over the group totals, in group order
+      const double e = __shfl_sync(FULL, D, g);
+      Ct = (g == (int)(t / GROUP_TILES)) ? C : Ct;
+      C = __dadd_rn(C, e);
+    }
+    const double total = C;
+    const double dt = __shfl_sync(FULL, Dt, (int)(t / GROUP_TILES));
+    if (threadIdx.x == 0) STAMP1(13);
+    for (int o = 16; o > 0; o >>= 1) gmin = min(gmin, __shfl_xor_sync(FULL, gmin, o));
+    if (lane == 0) {
+      s_C = Ct;
+      s_P = dt;
+      s_total = total;
+      s_min = gmin;
+    }
   }
   __syncthreads();
   const double Cg = s_C, P = s_P, total = s_total;

@@ -65,8 +65,8 @@ __global__ void k_ws_init(ScanHdr* h) {
 // (pass 1 left each tile's minimum in incl[t]) and the reference's
 // exactness trigger zmin <= 1e-14 T (randkit.py:95).
 constexpr int CHAIN_THREADS = 512;
-constexpr int64_t CHAIN_CHUNK = 64 * GROUP_TILES;  // tiles staged in shared memory per round
-constexpr int CHAIN_MAX_GROUPS = 4096;              // nt <= 2^20 tiles
+constexpr int64_t CHAIN_CHUNK = 16384;    // tiles staged in shared memory per round (a multiple of GROUP_TILES)
+constexpr int CHAIN_MAX_GROUPS = 8192;    // nt <= 2^18 tiles
 constexpr size_t CHAIN_SMEM = (size_t)CHAIN_CHUNK * 8 + (size_t)CHAIN_MAX_GROUPS * 8;
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64_t nt, int mode,
@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
     __syncthreads();
     // 2. one thread per group: serial left fold from shared memory
     const int64_t g0 = c0 / GROUP_TILES, g1 = cdiv(c1, GROUP_TILES);
+    static_assert(CHAIN_CHUNK % GROUP_TILES == 0, "chunks hold whole groups");
     for (int64_t g = g0 + threadIdx.x; g < g1; g += CHAIN_THREADS) {
       const int64_t t0 = g * GROUP_TILES - c0;
       const int64_t t1 = ((g + 1) * GROUP_TILES < c1 ? (g + 1) * GROUP_TILES : c1) - c0;

@@ -298,7 +298,7 @@ int dr_shard_unif_local(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, co
     return DRS_ERR_ARG;
   const int64_t nt = cdiv(n + 1, TSU);
   if (nt > ws_capacity_tiles(ws_bytes)) return DRS_ERR_WORKSPACE;
-  if (nt > (int64_t)4096 * GROUP_TILES) return DRS_ERR_ARG;
+  if (nt > (int64_t)8192 * GROUP_TILES) return DRS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const ScanWS s = carve_ws(ws, ws_bytes);
   PhiloxSpacings src{k0, k1, offset, nullptr};

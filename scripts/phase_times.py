@@ -18,7 +18,7 @@ sys.path.insert(0, str(ROOT))
 csrc = ROOT / "paper_2604_01356_b200" / "csrc"
 so = Path("/tmp/libdrs_prof.so")
 objs = []
-for f in ["drs_scan", "drs_match", "drs_batched", "drs_shard", "drs_fused"]:
+for f in sorted(x.stem for x in csrc.glob("*.cu")):
     o = f"/tmp/{f}_prof.o"
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler",
                     "-fPIC", "-DDRS_PHASE_TIMING", *os.environ.get("DRS_PROF_FLAGS", "").split(), "-c", str(csrc / f"{f}.cu"), "-o", o], check=True)
@@ -49,9 +49,12 @@ for rep in range(6):
     nt = (N + 1 + 511) // 512
     buf = np.zeros(nt * 16, dtype=np.uint64)
     L.dr_debug_phase_times(buf.ctypes.data, buf.size)
-    t = buf.reshape(nt, 16)[:, :9].astype(np.float64)
+    t = buf.reshape(nt, 16)[:, :14].astype(np.float64)
     rows.append(t - t[:, 0].min())
 t = rows[-1]
 print(f"{cfg}: {t.shape[0]} CTAs; times since first CTA start (us): median / max over CTAs")
 for k, nm in enumerate(names):
     print(f"  {k} {nm:14s} {np.median(t[:, k]) / 1e3:8.2f} {t[:, k].max() / 1e3:8.2f}")
+for k, nm in [(9, "all arrived"), (10, "fold start"), (11, "loads done"), (12, "group fold"), (13, "C fold")]:
+    if t[:, k].max() > 0:
+        print(f"  {k} {nm:14s} {np.median(t[:, k]) / 1e3:8.2f} {t[:, k].max() / 1e3:8.2f}")

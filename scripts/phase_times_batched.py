@@ -13,7 +13,7 @@ sys.path.insert(0, str(ROOT))
 csrc = ROOT / "paper_2604_01356_b200" / "csrc"
 so = Path("/tmp/libdrs_prof.so")
 objs = []
-for f in ["drs_scan", "drs_match", "drs_batched", "drs_shard", "drs_fused"]:
+for f in sorted(x.stem for x in csrc.glob("*.cu")):
     o = f"/tmp/{f}_prof.o"
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-Xcompiler",
                     "-fPIC", "-DDRS_PHASE_TIMING", *os.environ.get("DRS_PROF_FLAGS", "").split(), "-c",

@@ -40,7 +40,7 @@ def test_geometry_matches_oracle(orc):
     from paper_2604_01356_b200 import _lib
 
     lanes, warps, kt, ku, fan, grp = _lib.scan_geometry()
-    assert (lanes, warps, kt, ku, fan, grp) == (32, 8, 33, 2, 16, 256)
+    assert (lanes, warps, kt, ku, fan, grp) == (32, 8, 33, 2, 16, 32)
     M = 123457
     assert _lib.load_library().dr_index_entries(M) == orc.lib().drs_ref_index_entries(M)
 
