@@ -1,0 +1,159 @@
+"""the edge-case contract of the reference's public API,
+checked through the GPU package (names, messages, dtypes and draw accounting
+as in samplers.py / cdf.py / randkit.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _samplers(drs):
+    return {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}
+
+
+def test_n_zero_returns_empty_and_draws_nothing(drs):
+    """samplers.py:241-244, randkit.py:82-83"""
+    t = drs.build_weight_table([1.0, 2.0, 3.0])
+    for name, fn in _samplers(drs).items():
+        s = drs.RngStream(1)
+        out = fn(t, 0, s)
+        assert isinstance(out, np.ndarray) and out.dtype == np.int64 and out.shape == (0,), name
+        assert s.draws == 0, name
+    s = drs.RngStream(1)
+    u = drs.sorted_uniforms(s, 0)
+    assert u.shape == (0,) and u.dtype == np.float64 and s.draws == 0
+
+
+def test_draw_accounting(drs):
+    """n + 1 draws per sorted_uniforms / sorted sampler, n per binary_sampler (test_randkit.py:60-65)"""
+    t = drs.build_weight_table([1.0, 2.0, 3.0])
+    for name, fn in _samplers(drs).items():
+        s = drs.RngStream(2)
+        fn(t, 10, s)
+        assert s.draws == (10 if name == "binary" else 11), name
+
+
+def test_empty_u_to_matchers(drs):
+    """samplers.py:70-71, 173-174, 204-205"""
+    t = drs.build_weight_table([1.0, 1.0])
+    for fn in (drs.ccf_match, drs.dac_match):
+        out = fn(np.zeros(0), t)
+        assert out.dtype == np.int64 and out.shape == (0,)
+
+
+def test_negative_n(drs):
+    """randkit.py:80-81"""
+    with pytest.raises(ValueError, match="n must be >= 0"):
+        drs.sorted_uniforms(drs.RngStream(0), -1)
+    t = drs.build_weight_table([1.0])
+    for fn in (drs.dac_sampler, drs.ccf_sampler):
+        with pytest.raises(ValueError, match="n must be >= 0"):
+            fn(t, -1, drs.RngStream(0))
+
+
+@pytest.mark.parametrize("raw", [[], np.zeros((2, 3)), np.zeros((0,))])
+def test_empty_or_2d_weights(drs, raw):
+    """cdf.py:72-73: the same message for a 2-D array"""
+    with pytest.raises(ValueError, match="empty distribution"):
+        drs.build_weight_table(raw)
+
+
+def test_trailing_and_leading_zero_weights(drs):
+    """cdf.py:85-88 and the lower-bound tie rule samplers.py:86; SPEC.md:118"""
+    t = drs.build_weight_table([1.0, 0.0, 0.0])
+    np.testing.assert_array_equal(t.cum, [1.0, 1.0, 1.0])
+    np.testing.assert_array_equal(drs.dac_match([1.0], t), [0])
+    np.testing.assert_array_equal(drs.ccf_match([1.0], t), [0])
+    t = drs.build_weight_table([0.0, 1.0])
+    np.testing.assert_array_equal(t.cum, [0.0, 1.0])
+    for fn in _samplers(drs).values():
+        assert np.all(fn(t, 1000, drs.RngStream(3)) == 1)
+
+
+def test_u_equal_one_maps_to_first_full_index(drs):
+    """SPEC.md:221, cdf.py:88"""
+    t = drs.build_weight_table([1.0, 2.0, 0.0, 0.0])
+    for fn in (drs.ccf_match, drs.dac_match):
+        np.testing.assert_array_equal(fn([0.5, 1.0], t), [1, 1])
+    assert drs.linear_oracle(t, 1.0) == 1
+
+
+def test_duplicate_u_check_and_no_check(drs):
+    """samplers.py:74-75 (check=True) versus the sampler path (check=False)"""
+    t = drs.build_weight_table([1.0, 1.0, 1.0])
+    u = [0.2, 0.5, 0.5, 0.9]
+    for fn in (drs.ccf_match, drs.dac_match):
+        with pytest.raises(ValueError, match="input not sorted"):
+            fn(u, t)
+        np.testing.assert_array_equal(fn(u, t, check=False), [0, 1, 1, 2])
+
+
+def test_out_of_support_u(drs):
+    """samplers.py:72-73, 57"""
+    t = drs.build_weight_table([1.0, 1.0])
+    for fn in (drs.ccf_match, drs.dac_match):
+        with pytest.raises(ValueError, match=r"uniforms must lie in \(0, 1\]"):
+            fn([0.0, 0.5], t)
+        with pytest.raises(ValueError, match=r"uniforms must lie in \(0, 1\]"):
+            fn([0.5, 1.5], t)
+    for bad in (0.0, 1.5, -1.0):
+        with pytest.raises(ValueError, match=r"u must lie in \(0, 1\]"):
+            drs.linear_oracle(t, bad)
+
+
+def test_array_like_inputs(drs):
+    """cdf.py:71, samplers.py:168,199: lists are coerced to contiguous float64"""
+    t = drs.build_weight_table([2, 1, 1])  # ints
+    np.testing.assert_array_equal(t.cum, [0.5, 0.75, 1.0])
+    np.testing.assert_array_equal(drs.dac_match([0.1, 0.6, 0.8], drs.WeightTable([0.25, 0.5, 0.75, 1.0])), [0, 2, 3])
+
+
+def test_weight_table_top_entry(drs):
+    """cdf.py:39-40"""
+    with pytest.raises(ValueError, match="cumulative weights must end at exactly 1"):
+        drs.WeightTable([0.5, 0.9])
+    with pytest.raises(ValueError, match="cumulative weights must be non-decreasing from >= 0"):
+        drs.WeightTable([0.5, 0.4, 1.0])
+    assert drs.build_weight_table(np.exp(np.random.default_rng(0).standard_normal(1000))).cum[-1] == 1.0
+
+
+def test_output_dtype_and_order(drs):
+    """samplers.py:172,203,242; int64, matchers and sorted
+    samplers non-decreasing, binary_sampler in draw order"""
+    t = drs.build_weight_table(np.exp(np.random.default_rng(1).standard_normal(5000)))
+    for name, fn in _samplers(drs).items():
+        out = fn(t, 4000, drs.RngStream(9))
+        assert out.dtype == np.int64 and out.min() >= 0 and out.max() < 5000
+        if name != "binary":
+            assert np.all(np.diff(out) >= 0), name
+    b = drs.binary_sampler(t, 4000, drs.RngStream(9))
+    assert not np.all(np.diff(b) >= 0)  # draw order, not sorted
+
+
+def test_upper_bound_search_errors(drs):
+    """cdf.py:103-107"""
+    t = drs.build_weight_table([1.0, 1.0, 1.0])
+    with pytest.raises(ValueError, match="empty range"):
+        drs.upper_bound_search(t, 2, 1, 0.5)
+    with pytest.raises(IndexError):
+        drs.upper_bound_search(t, 0, 3, 0.5)
+    assert drs.upper_bound_search(t, 0, 2, 0.5) == 1
+
+
+def test_stats_raises_instead_of_cpu_fallback(drs):
+    t = drs.build_weight_table([1.0, 1.0])
+    with pytest.raises(NotImplementedError):
+        drs.dac_sampler(t, 4, drs.RngStream(0), stats=drs.OpStats())
+    with pytest.raises(NotImplementedError):
+        drs.ccf_match([0.5], t, stats=drs.OpStats())
+
+
+def test_device_in_device_out(drs):
+    t = drs.build_weight_table(torch.rand(100, dtype=torch.float64, device="cuda") + 0.1)
+    u = torch.sort(torch.rand(50, dtype=torch.float64, device="cuda"))[0]
+    out = drs.dac_match(u, t)
+    assert isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.int64
+    out = drs.dac_sampler(t, 50, drs.RngStream(1), device=True)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
