@@ -105,6 +105,17 @@ __device__ __forceinline__ int warp_count_le_smem(const double* a, int n, double
 // merge path -- every thread takes an equal diagonal segment, locates its
 // start by bisection and merges branch-free, taking W before u only when
 // W < u, so each u gets the first j with W[j] >= u.
+// first p in [0, n) with a[p] >= x, clamped to n-1 (the reference's bisection)
+__device__ __forceinline__ int smem_lower_bound(const double* a, int n, double x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int m = (lo + hi) >> 1;
+    if (a[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  return lo;
+}
+
 constexpr int MT_THREADS = 256;
 constexpr int MT_TW = 4096;   // max W entries per tile (32 KB)
 constexpr int MT_UC = 1024;   // u's staged per merge-path chunk (8 KB)
@@ -118,6 +129,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   int64_t* so = (int64_t*)(su + MT_UC);  // [MT_UC] results, written out coalesced
   __shared__ __align__(8) uint64_t bar;
   __shared__ int64_t s_ib, s_ie;
+  __shared__ int s_w0, s_w1;
   const int64_t t = blockIdx.x;
   const int64_t j0 = t * tw;
   const int len = (int)((M - j0) < tw ? (M - j0) : tw);
@@ -157,23 +169,34 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
     const int c = (int)((ie - c0) < MT_UC ? (ie - c0) : MT_UC);
     for (int i = threadIdx.x; i < c; i += MT_THREADS) su[i] = __ldg(U + c0 + i);
     __syncthreads();
-    const int total = len + c;
+    // the chunk's u's land in sw[wa0 .. wa1] (wa0 = lower bound of its first
+    // u, wa1 of its last): merge only that part of the tile
+    if (threadIdx.x < 2) {
+      const int v = smem_lower_bound(sw, len, su[threadIdx.x == 0 ? 0 : c - 1]);
+      if (threadIdx.x == 0) s_w0 = v;
+      else s_w1 = v;
+    }
+    __syncthreads();
+    const int wa0 = s_w0;
+    const int wl = s_w1 - wa0 + 1;  // W entries in the merge
+    const double* sws = sw + wa0;
+    const int total = wl + c;
     const int per = (total + MT_THREADS - 1) / MT_THREADS;
     const int d0 = min(total, (int)threadIdx.x * per), d1 = min(total, d0 + per);
-    int lo = max(0, d0 - c), hi = min(d0, len);
+    int lo = max(0, d0 - c), hi = min(d0, wl);
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (sw[mid] < su[d0 - mid - 1]) lo = mid + 1;
+      if (sws[mid] < su[d0 - mid - 1]) lo = mid + 1;
       else hi = mid;
     }
     int ia = lo, ibb = d0 - lo;
     for (int d = d0; d < d1; ++d) {
-      const double wa = (ia < len) ? sw[ia] : dinf();
+      const double wa = (ia < wl) ? sws[ia] : dinf();
       const double xb = (ibb < c) ? su[ibb] : dinf();
-      if (ibb >= c || (ia < len && wa < xb)) {
+      if (ibb >= c || (ia < wl && wa < xb)) {
         ++ia;
       } else {
-        so[ibb] = j0 + (ia < len ? ia : len - 1);  // clamp (u > 1 only without check)
+        so[ibb] = j0 + wa0 + (ia < wl ? ia : wl - 1);  // clamp (u > 1 only without check)
         ++ibb;
       }
     }
