@@ -218,12 +218,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   // not queue behind these bulk transfers
   if (threadIdx.x == THREADS - 32) {
     mbar_init(&bar, 1);
-#if defined(DRS_EXP_NO_STAGE)
-    mbar_expect_tx(&bar, 0);  // experiment: no index staging
-#else
     mbar_expect_tx(&bar, sbytes);
     if (sbytes) bulk_g2s(sidx, a.idx + a.sl.base, sbytes, &bar);
-#endif
     const int64_t lvl = (a.sl.k_smem >= 2) ? a.sl.base - a.d.off[a.sl.k_smem - 1] : 0;  // doubles
     const int64_t cap = lvl < L2_PREFETCH_DOUBLES ? lvl : L2_PREFETCH_DOUBLES;
     const int64_t plo = a.sl.base - cap;
