@@ -78,32 +78,6 @@ __device__ __forceinline__ int count_lt16_smem(const double* p, double x) {
   return c;
 }
 
-// index_lower_bound with the top levels in shared memory
-__device__ __forceinline__ int64_t search_sm(const double* __restrict__ W, const double* __restrict__ idx,
-                                             const double* sidx, const IndexDesc& d, const SmemLevels& sl,
-                                             double x) {
-  int64_t b = 0;
-  for (int k = d.levels; k >= 1; --k) {
-    int c;
-    if (k >= sl.k_smem) c = count_lt16_smem(sidx + (d.off[k] - sl.base) + FANOUT * b, x);
-    else c = count_lt16(idx + d.off[k] + FANOUT * b, x);
-    const int64_t valid = d.n[k] - FANOUT * b;
-    if (c >= valid) c = (int)valid - 1;
-    b = FANOUT * b + c;
-  }
-  const int64_t j0 = FANOUT * b;
-  const int64_t valid = d.n[0] - j0;
-  int c;
-  if (valid >= FANOUT) {
-    c = count_lt16(W + j0, x);
-  } else {
-    c = 0;
-    for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x) ? 1 : 0;
-  }
-  if (c >= valid) c = (int)valid - 1;
-  return j0 + c;
-}
-
 // K_UNIF independent searches in lock-step: the level loop is outside, so the
 // lines of a level are in flight together
 __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const double* __restrict__ idx,
@@ -421,7 +395,23 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   }
 }
 
-// binary_sampler with the top index levels staged in shared memory
+// binary_sampler: persistent CTAs stage the top index levels in shared memory
+// once (TMA) and loop over chunks of 2 x 256 draws; a warp's 32 consecutive
+// draws come from <= 9 Philox blocks computed by lanes 0..8 and shuffled;
+// each thread then runs its two 16-ary searches in lock-step
+__device__ __forceinline__ uint64_t warp_raw_draw(uint64_t k0, uint64_t k1, uint64_t d0) {
+  const int lane = threadIdx.x & 31;  // lane's draw: d0 + lane
+  const uint64_t b0 = d0 >> 2;
+  U64x4 v{0, 0, 0, 0};
+  if (lane < 9) v = philox_block(k0, k1, b0 + (uint64_t)lane);
+  const uint64_t dd = d0 + (uint64_t)lane;
+  const int src = (int)((dd >> 2) - b0);
+  const uint64_t w0 = __shfl_sync(FULL, v.w0, src), w1 = __shfl_sync(FULL, v.w1, src);
+  const uint64_t w2 = __shfl_sync(FULL, v.w2, src), w3 = __shfl_sync(FULL, v.w3, src);
+  const int wi = (int)(dd & 3);
+  return wi == 0 ? w0 : (wi == 1 ? w1 : (wi == 2 ? w2 : w3));
+}
+
 __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restrict__ W,
                                                           const double* __restrict__ idx, IndexDesc d,
                                                           SmemLevels sl, uint64_t k0, uint64_t k1,
@@ -437,21 +427,28 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) - lane;
   const uint64_t off = offset_dev ? *(volatile uint64_t*)offset_dev : offset;
-  const uint64_t d0 = off + (uint64_t)base;
-  const uint64_t b0 = d0 >> 2;
-  U64x4 v{0, 0, 0, 0};
-  if (lane < 9) v = philox_block(k0, k1, b0 + (uint64_t)lane);
-  const uint64_t dd = d0 + (uint64_t)lane;
-  const int src = (int)((dd >> 2) - b0);
-  const uint64_t w0 = __shfl_sync(FULL, v.w0, src), w1 = __shfl_sync(FULL, v.w1, src);
-  const uint64_t w2 = __shfl_sync(FULL, v.w2, src), w3 = __shfl_sync(FULL, v.w3, src);
-  const int wi = (int)(dd & 3);
-  const uint64_t raw = wi == 0 ? w0 : (wi == 1 ? w1 : (wi == 2 ? w2 : w3));
-  mbar_wait(&bar, 0);
-  const int64_t i = base + lane;
-  if (i < N) out[i] = search_sm(W, idx, sidx, d, sl, u01(raw));
+  bool staged = false;
+  static_assert(K_UNIF == 2, "two draws per thread per chunk");
+  for (int64_t base = (int64_t)blockIdx.x * 2 * blockDim.x; base < N; base += (int64_t)gridDim.x * 2 * blockDim.x) {
+    double u[K_UNIF];
+    int64_t i[K_UNIF];
+#pragma unroll
+    for (int h = 0; h < K_UNIF; ++h) {
+      const int64_t w0 = base + h * blockDim.x + threadIdx.x - lane;  // the warp's first draw
+      i[h] = w0 + lane;
+      u[h] = u01(warp_raw_draw(k0, k1, off + (uint64_t)w0));
+    }
+    if (!staged) {
+      mbar_wait(&bar, 0);
+      staged = true;
+    }
+    int64_t r[K_UNIF];
+    search_k_sm(W, idx, sidx, d, sl, u, r);
+#pragma unroll
+    for (int h = 0; h < K_UNIF; ++h)
+      if (i[h] < N) out[i[h]] = r[h];
+  }
 }
 
 __global__ void k_advance_offset(uint64_t* p, uint64_t by) { *p += by; }
@@ -549,13 +546,26 @@ int dr_sample_binary_dev(const double* W, const double* idx, int64_t M, uint64_t
   const IndexDesc d = make_index_desc(M);
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
   const SmemLevels sl = plan_smem_levels(d);
-  static bool attr = false;
-  if (!attr) {
+  // persistent grid: as many CTAs as fit with this shared-memory size
+  static int sms = 0;
+  static size_t c_smem = (size_t)-1;
+  static int c_per = 0;
+  const size_t smem = (size_t)sl.count * 8;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(k_sample_binary_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
-    attr = true;
   }
-  k_sample_binary_sm<<<(unsigned)cdiv(N, 256), 256, (size_t)sl.count * 8, (cudaStream_t)stream>>>(
-      W, idx, d, sl, k0, k1, offset, offset_dev, N, out);
+  if (c_smem != smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, k_sample_binary_sm, 256, smem);
+    c_smem = smem;
+    if (c_per < 1) c_per = 1;
+  }
+  const int64_t chunks = cdiv(N, 512);
+  const int64_t grid = chunks < (int64_t)sms * c_per ? chunks : (int64_t)sms * c_per;
+  k_sample_binary_sm<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(W, idx, d, sl, k0, k1, offset,
+                                                                          offset_dev, N, out);
   if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
   if (offset_dev) k_advance_offset<<<1, 1, 0, (cudaStream_t)stream>>>(offset_dev, (uint64_t)N);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
