@@ -54,12 +54,12 @@ struct SmemLevels {
   int64_t count;    // doubles staged
 };
 
-SmemLevels plan_smem_levels(const IndexDesc& d) {
+SmemLevels plan_smem_levels(const IndexDesc& d, int64_t cap = SIDX_CAP) {
   SmemLevels s{d.levels + 1, 0, 0};
   if (d.levels == 0) return s;
   const int64_t end = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
   for (int k = d.levels; k >= 1; --k) {
-    if (end - d.off[k] > SIDX_CAP) break;
+    if (end - d.off[k] > cap) break;
     s.k_smem = k;
     s.base = d.off[k];
     s.count = end - d.off[k];
@@ -449,6 +449,66 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
     for (int h = 0; h < K_UNIF; ++h)
       if (i[h] < N) out[i[h]] = r[h];
   }
+}
+
+// dr_match_dac (search mode) / dr_match_binary on given u's: persistent CTAs
+// stage the top index levels once (capped so that several CTAs share an SM)
+// and run two lock-step searches per thread over coalesced chunks of u
+#ifndef DRS_MATCH_SMEM_CAP
+#define DRS_MATCH_SMEM_CAP 2048
+#endif
+__global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict__ W, const double* __restrict__ idx,
+                                                        IndexDesc d, SmemLevels sl, const double* __restrict__ u,
+                                                        int64_t N, int64_t* __restrict__ out) {
+  extern __shared__ __align__(128) double sidx[];
+  __shared__ __align__(8) uint64_t bar;
+  const uint32_t sbytes = (uint32_t)(sl.count * 8);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, sbytes);
+    if (sbytes) bulk_g2s(sidx, idx + sl.base, sbytes, &bar);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  for (int64_t base = (int64_t)blockIdx.x * 2 * blockDim.x; base < N; base += (int64_t)gridDim.x * 2 * blockDim.x) {
+    double x[K_UNIF];
+    int64_t i[K_UNIF];
+#pragma unroll
+    for (int h = 0; h < K_UNIF; ++h) {
+      i[h] = base + h * blockDim.x + threadIdx.x;
+      x[h] = (i[h] < N) ? __ldg(u + i[h]) : 0.5;
+    }
+    int64_t r[K_UNIF];
+    search_k_sm(W, idx, sidx, d, sl, x, r);
+#pragma unroll
+    for (int h = 0; h < K_UNIF; ++h)
+      if (i[h] < N) out[i[h]] = r[h];
+  }
+}
+
+int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,
+                    cudaStream_t st) {
+  const IndexDesc d = make_index_desc(M);
+  const SmemLevels sl = plan_smem_levels(d, DRS_MATCH_SMEM_CAP);
+  static int sms = 0;
+  static size_t c_smem = (size_t)-1;
+  static int c_per = 0;
+  const size_t smem = (size_t)sl.count * 8;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_match_index_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
+  }
+  if (c_smem != smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, k_match_index_sm, 256, smem);
+    c_smem = smem;
+    if (c_per < 1) c_per = 1;
+  }
+  const int64_t chunks = cdiv(N, 512);
+  const int64_t grid = chunks < (int64_t)sms * c_per ? chunks : (int64_t)sms * c_per;
+  k_match_index_sm<<<(unsigned)grid, 256, smem, st>>>(W, idx, d, sl, u, N, out);
+  return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 
 __global__ void k_advance_offset(uint64_t* p, uint64_t by) { *p += by; }

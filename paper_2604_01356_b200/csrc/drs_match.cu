@@ -293,9 +293,13 @@ int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st)
   return launch_rc();
 }
 
+int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,
+                    cudaStream_t st);  // drs_fused.cu
+
 int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
                         int64_t* out, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
+  if (d.levels > 0) return launch_index_sm(W, idx, M, u, N, out, st);
   k_match_index<<<(unsigned)cdiv(N, 256), 256, 0, st>>>(W, idx, d, u, N, out);
   return launch_rc();
 }
