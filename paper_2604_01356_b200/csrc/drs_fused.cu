@@ -457,9 +457,12 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
 #ifndef DRS_MATCH_SMEM_CAP
 #define DRS_MATCH_SMEM_CAP 2048
 #endif
+// rng (optional, on the device): search only u[rng[0] .. rng[1]) and add
+// `shift` to the indices (a W shard of a sharded table)
 __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict__ W, const double* __restrict__ idx,
                                                         IndexDesc d, SmemLevels sl, const double* __restrict__ u,
-                                                        int64_t N, int64_t* __restrict__ out) {
+                                                        int64_t N, int64_t* __restrict__ out,
+                                                        const int64_t* __restrict__ rng, int64_t shift) {
   extern __shared__ __align__(128) double sidx[];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t sbytes = (uint32_t)(sl.count * 8);
@@ -470,24 +473,25 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  for (int64_t base = (int64_t)blockIdx.x * 2 * blockDim.x; base < N; base += (int64_t)gridDim.x * 2 * blockDim.x) {
+  const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
+  for (int64_t base = lo + (int64_t)blockIdx.x * 2 * blockDim.x; base < hi; base += (int64_t)gridDim.x * 2 * blockDim.x) {
     double x[K_UNIF];
     int64_t i[K_UNIF];
 #pragma unroll
     for (int h = 0; h < K_UNIF; ++h) {
       i[h] = base + h * blockDim.x + threadIdx.x;
-      x[h] = (i[h] < N) ? __ldg(u + i[h]) : 0.5;
+      x[h] = (i[h] < hi) ? __ldg(u + i[h]) : 0.5;
     }
     int64_t r[K_UNIF];
     search_k_sm(W, idx, sidx, d, sl, x, r);
 #pragma unroll
     for (int h = 0; h < K_UNIF; ++h)
-      if (i[h] < N) out[i[h]] = r[h];
+      if (i[h] < hi) out[i[h]] = shift + r[h];
   }
 }
 
 int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,
-                    cudaStream_t st) {
+                    cudaStream_t st, const int64_t* rng, int64_t shift) {
   const IndexDesc d = make_index_desc(M);
   const SmemLevels sl = plan_smem_levels(d, DRS_MATCH_SMEM_CAP);
   static int sms = 0;
@@ -507,7 +511,7 @@ int launch_index_sm(const double* W, const double* idx, int64_t M, const double*
   }
   const int64_t chunks = cdiv(N, 512);
   const int64_t grid = chunks < (int64_t)sms * c_per ? chunks : (int64_t)sms * c_per;
-  k_match_index_sm<<<(unsigned)grid, 256, smem, st>>>(W, idx, d, sl, u, N, out);
+  k_match_index_sm<<<(unsigned)grid, 256, smem, st>>>(W, idx, d, sl, u, N, out, rng, shift);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 

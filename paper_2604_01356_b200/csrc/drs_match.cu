@@ -294,7 +294,7 @@ int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st)
 }
 
 int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,
-                    cudaStream_t st);  // drs_fused.cu
+                    cudaStream_t st, const int64_t* rng = nullptr, int64_t shift = 0);  // drs_fused.cu
 
 int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
                         int64_t* out, cudaStream_t st) {

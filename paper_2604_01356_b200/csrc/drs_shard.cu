@@ -13,6 +13,8 @@ namespace drs {
 
 IndexDesc make_index_desc(int64_t M);
 int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st);
+int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,
+                    cudaStream_t st, const int64_t* rng, int64_t shift);
 void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total, cudaStream_t st);
 int64_t ws_capacity_tiles(size_t ws_bytes);
 ScanWS carve_ws(void* ws, size_t ws_bytes);
@@ -275,6 +277,7 @@ int dr_shard_match(const double* W, const double* idx, int64_t Mg, int64_t shard
   if (N == 0) return DRS_OK;
   const IndexDesc d = make_index_desc(Mg);
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
+  if (d.levels > 0) return launch_index_sm(W, idx, Mg, U, N, out, (cudaStream_t)stream, range, shard_start);
   const int64_t blocks = cdiv(N, 256) < 148 * 16 ? cdiv(N, 256) : 148 * 16;
   k_shard_match<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(W, idx, d, shard_start, U, range, out);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
