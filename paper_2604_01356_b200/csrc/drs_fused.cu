@@ -173,10 +173,12 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   __shared__ unsigned long long s_min;
   __shared__ uint32_t s_flag;
   __shared__ uint64_t s_words[PhiloxSpacings::SMEM_WORDS];
+  __shared__ double s_agg[FUSED_MAX_TILES + FUSED_MAX_TILES / 32 + 256 + 8];  // padded tile totals
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = blockIdx.x;
   const int64_t nt = gridDim.x;
   const int64_t n = a.n;
+  if (threadIdx.x == 0) STAMP1(10);  // entry
   uint32_t* bcount = &a.ws.hdr->bar_count;
   uint32_t* bgen = &a.ws.hdr->bar_gen;
 
@@ -242,37 +244,43 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   if (threadIdx.x == 0) {
     st_relaxed_f64(&a.ws.agg[t], A);
     st_relaxed_f64(&a.ws.incl[t], __longlong_as_double((long long)s_min));
-    __threadfence();
-    atomicAdd(cnt + (gen & 1), 1ull);
-    while (ld_acquire_u64(cnt + (gen & 1)) < (unsigned long long)nt) __nanosleep(64);
+    red_release_add_u64(cnt + (gen & 1), 1ull);
+    while (ld_acquire_u64(cnt + (gen & 1)) < (unsigned long long)nt) {
+    }
   }
   __syncthreads();
   STAMP(9);
   if (warp == 0) {
-    // lane g folds group g (tiles 32g .. 32g+31) serially; lane 0 then folds
-    // the group totals: a 32 + ng step chain instead of nt steps
+    // the nt totals and minima arrive by coalesced L2 loads (.cg: no stale
+    // L1 copies of the previous call's values) into shared memory, padded
+    // one slot per 32 so that lane g then reads group g (tiles 32g .. 32g+31)
+    // conflict-free and folds it serially; the group totals are folded in
+    // group order below: a 32 + ng step chain instead of nt steps
     static_assert(GROUP_TILES == 32, "one lane per group of 32 tiles");
     unsigned long long gmin = 0x7FF0000000000000ULL;
-    double D = 0.0, Dt = 0.0;
-    const int64_t gb = (int64_t)lane * GROUP_TILES;
-    if (threadIdx.x == 0) STAMP1(10);
-    if (gb < nt) {
-      double v[GROUP_TILES];
-      // L2 loads (.cg: no stale L1 copies of the previous call's values), all
-      // issued before the first use
-      double m[GROUP_TILES];
+    for (int64_t k0 = 0; k0 < nt; k0 += 8 * 32) {
+      double v[8], m[8];
 #pragma unroll
-      for (int k = 0; k < GROUP_TILES; ++k) {
-        v[k] = (gb + k < nt) ? __ldcg(&a.ws.agg[gb + k]) : 0.0;
-        m[k] = (gb + k < nt) ? __ldcg(&a.ws.incl[gb + k]) : __longlong_as_double(0x7FF0000000000000LL);
+      for (int q = 0; q < 8; ++q) {
+        const int64_t k = k0 + q * 32 + lane;
+        v[q] = (k < nt) ? __ldcg(&a.ws.agg[k]) : 0.0;
+        m[q] = (k < nt) ? __ldcg(&a.ws.incl[k]) : __longlong_as_double(0x7FF0000000000000LL);
       }
 #pragma unroll
-      for (int k = 0; k < GROUP_TILES; ++k) gmin = min(gmin, (unsigned long long)__double_as_longlong(m[k]));
-      if (threadIdx.x == 0) STAMP1(11);
+      for (int q = 0; q < 8; ++q) {
+        const int64_t k = k0 + q * 32 + lane;
+        s_agg[k + (k >> 5)] = v[q];  // tiles past nt hold +0.0: the folds are unchanged
+        gmin = min(gmin, (unsigned long long)__double_as_longlong(m[q]));
+      }
+    }
+    __syncwarp();
+    double D = 0.0, Dt = 0.0;
+    const int64_t gb = (int64_t)lane * GROUP_TILES;
+    if (gb < nt) {
 #pragma unroll
       for (int k = 0; k < GROUP_TILES; ++k) {
         Dt = (gb + k == t) ? D : Dt;
-        D = __dadd_rn(D, v[k]);  // tiles past nt add +0.0: the fold is unchanged
+        D = __dadd_rn(D, s_agg[gb + k + lane]);
       }
     }
     if (t == 0 && lane == 0) {
@@ -281,7 +289,6 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
       cnt[(gen + 1) & 1] = 0ull;  // the next call's counter
       a.ws.hdr->fgen = gen + 1;
     }
-    if (threadIdx.x == 0) STAMP1(12);
     const int ng = (int)cdiv(nt, GROUP_TILES);
     double C = 0.0, Ct = 0.0;
     for (int g = 0; g < ng; ++g) {  // C over the group totals, in group order
