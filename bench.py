@@ -357,7 +357,8 @@ def run_drs(args, rank, world, local_rank):
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "kernel_ms": kernel_ms, "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": alg_bytes},
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "physical_frac": (traffic / (kernel_ms * 1e-3) / 1e9 / peak) if traffic else None},
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "table_build": table_build,
