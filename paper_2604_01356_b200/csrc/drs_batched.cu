@@ -11,7 +11,8 @@
 //     others' compute);
 //   * while the copy is in flight it generates and scans the N_f + 1 Philox
 //     spacings (they do not depend on w; every CTA of the cluster derives the
-//     same U, exactly as dr_sorted_uniforms does);
+//     same U, exactly as dr_sorted_uniforms does; with N_f + 1 <= 512 each
+//     Philox block is computed once, by one thread);
 //   * ONE sweep over the tile: each lane folds its K_TABLE-element chunk
 //     serially (validating from the high words in the integer pipe), writes
 //     the chunk-local prefix s2 in place, and the CTA folds lane and warp
@@ -54,6 +55,28 @@ __device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, dou
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
 }
 
+// the exactness check and repair of randkit.py:95-116 on a filter's U (in
+// shared memory), by thread 0 and serially: rare, and N_f is small
+__device__ __forceinline__ void uniform_repair(double* su, int64_t Nf, unsigned long long smin, double total,
+                                               int r, int32_t* status) {
+  const double zmin = __longlong_as_double((long long)smin);
+  if (threadIdx.x != 0 || zmin > __dmul_rn(1e-14, total)) return;
+  bool b2 = (su[0] <= 0.0) || (su[Nf - 1] >= 1.0);
+  for (int64_t i = 1; !b2 && i < Nf; ++i) b2 = !(__dsub_rn(su[i], su[i - 1]) > 0.0);
+  if (!b2) return;
+  double lo = 0.0;
+  for (int64_t i = 0; i < Nf; ++i) {
+    if (su[i] <= lo) su[i] = nextafter(lo, 1.0);
+    lo = su[i];
+  }
+  double hi = 1.0;
+  for (int64_t i = Nf - 1; i >= 0; --i) {
+    if (su[i] >= hi) su[i] = nextafter(hi, 0.0);
+    hi = su[i];
+  }
+  if (r == 0) atomicOr(status, DRS_ST_REPAIRED);
+}
+
 // valid weight <=> 0 <= x < inf (-0.0 included, NaN excluded); screened from
 // the high word: any sign bit (exact re-check follows) or an all-ones exponent
 __device__ __forceinline__ void track_hi(double x, uint32_t& any_sign, uint32_t& max_mag) {
@@ -77,14 +100,14 @@ struct BatchedArgs {
 __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
-  __shared__ FoldSmem fst;        // fold of the table tile
-  __shared__ FoldSmem fsu;        // fold of a uniform tile
+  __shared__ FoldSmem fs;         // fold of a uniform tile, then of the table tile
   __shared__ double s_R[WARPS];   // warp bases R of the table tile
   __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
   __shared__ double s_Au[MAX_UT];
   __shared__ unsigned long long s_min;
   __shared__ int s_bad;
   __shared__ int s_range[2];
+  __shared__ double s_cend[THREADS];  // S at each lane chunk's last entry
   const int64_t Mf = a.Mf, Nf = a.Nf, ne = Nf + 1;
   const int r = (int)cluster_rank();
   const int64_t f = blockIdx.x / a.ntt;
@@ -124,7 +147,28 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
       double z[K_UNIF];
 #pragma unroll
       for (int i = 0; i < K_UNIF; ++i) z[i] = 0.0;
-      if (e0 < ne) {
+      if (a.ntu == 1) {
+        // one tile: each Philox block is computed once, by one thread, into
+        // su (sized for it; su is written only after these words are read)
+        uint64_t* words = reinterpret_cast<uint64_t*>(su);
+        const uint64_t b0 = off >> 2;
+        const int nblk = (int)(((off + (uint64_t)ne - 1) >> 2) - b0 + 1);
+        for (int blk = threadIdx.x; blk < nblk; blk += THREADS) {
+          const U64x4 v = philox_block(k0, k1, b0 + (uint64_t)blk);
+          words[4 * blk + 0] = v.w0; words[4 * blk + 1] = v.w1;
+          words[4 * blk + 2] = v.w2; words[4 * blk + 3] = v.w3;
+        }
+        __syncthreads();
+        const int a0 = (int)(off & 3);
+#pragma unroll
+        for (int i = 0; i < K_UNIF; ++i) {
+          if (e0 + i < ne) {
+            z[i] = neglog(u01(words[a0 + e0 + i]));
+            mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
+          }
+        }
+        __syncthreads();  // words read before su is written
+      } else if (e0 < ne) {
         const uint64_t d0 = off + (uint64_t)e0;
         const uint64_t b0 = d0 >> 2, b1 = (d0 + K_UNIF - 1) >> 2;
         const U64x4 v0 = philox_block(k0, k1, b0);
@@ -145,12 +189,12 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
 #pragma unroll
       for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
       double Q, R;
-      const double A = block_fold(sc[K_UNIF - 1], fsu, Q, R);
+      const double A = block_fold(sc[K_UNIF - 1], fs, Q, R);
       if (threadIdx.x == 0) s_Au[t] = A;
 #pragma unroll
       for (int i = 0; i < K_UNIF; ++i)
         if (e0 + i < ne) su[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
-      __syncthreads();  // fsu reuse
+      __syncthreads();  // fs reuse
     }
     if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
     double Pu[MAX_UT];
@@ -168,25 +212,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
       su[i] = __ddiv_rn(__dadd_rn(p, su[i]), total);
     }
     __syncthreads();
-    const double zmin = __longlong_as_double((long long)s_min);
-    if (!(zmin > __dmul_rn(1e-14, total)) && threadIdx.x == 0) {
-      // the exactness check and repair of randkit.py:95-116, serially: rare, Nf small
-      bool b2 = (su[0] <= 0.0) || (su[Nf - 1] >= 1.0);
-      for (int64_t i = 1; !b2 && i < Nf; ++i) b2 = !(__dsub_rn(su[i], su[i - 1]) > 0.0);
-      if (b2) {
-        double lo = 0.0;
-        for (int64_t i = 0; i < Nf; ++i) {
-          if (su[i] <= lo) su[i] = nextafter(lo, 1.0);
-          lo = su[i];
-        }
-        double hi = 1.0;
-        for (int64_t i = Nf - 1; i >= 0; --i) {
-          if (su[i] >= hi) su[i] = nextafter(hi, 0.0);
-          hi = su[i];
-        }
-        if (r == 0) atomicOr(a.status, DRS_ST_REPAIRED);
-      }
-    }
+    uniform_repair(su, Nf, s_min, total, r, a.status);
   }
 
   // ---- 2. the table sweep over this CTA's tile
@@ -218,7 +244,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   if (any_sign & 0x80000000u)         // a sign bit: re-check the raw weights (-0.0 is valid)
     for (int i = 0; i < K_TABLE && c0 + i < len; ++i) bad |= !(wt[c0 + i] >= 0.0);
   double Q, R;
-  const double A = block_fold(s, fst, Q, R);
+  const double A = block_fold(s, fs, Q, R);
   sQ[threadIdx.x] = Q;
   if (lane == 0) s_R[warp] = R;
   if (bad) s_bad = 1;
@@ -235,6 +261,12 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
     T = __dadd_rn(T, s_A[q]);
   }
   const double Pnext = __dadd_rn(Pr, s_A[r]);  // == S at the tile's last entry
+  // S at the end of every lane chunk (the search's first level)
+  {
+    const int lastc = (c0 + K_TABLE <= len) ? K_TABLE - 1 : len - 1 - c0;
+    s_cend[threadIdx.x] = (lastc >= 0) ? __dadd_rn(Pr, __dadd_rn(s_R[warp], __dadd_rn(Q, chunk[lastc]))) : dinf();
+  }
+  __syncthreads();
   STAMP(4);
   if (threadIdx.x == 0) {
     int st = s_bad ? DRS_ST_INVALID_WEIGHT : 0;
@@ -284,11 +316,21 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
       } else {
         do sx = nextafter(sx, dinf()); while (__ddiv_rn(sx, T) < x);
       }
-      int lo = 0, hi = len - 1;
+      // the chunk: first chunk whose last S is >= s*(x) (the tile's last
+      // chunk otherwise), then the entry inside it
+      const int nch = (len + K_TABLE - 1) / K_TABLE;
+      int clo = 0, chi = nch - 1;
+      while (clo < chi) {
+        const int m = (clo + chi) >> 1;
+        if (s_cend[m] < sx) clo = m + 1;
+        else chi = m;
+      }
+      const double Rc = s_R[clo >> 5], Qc = sQ[clo];
+      const int cb = clo * K_TABLE;
+      int lo = cb, hi = min(cb + K_TABLE, len) - 1;
       while (lo < hi) {
         const int m = (lo + hi) >> 1;
-        const int c = m / K_TABLE;
-        const double S = __dadd_rn(Pr, __dadd_rn(s_R[c >> 5], __dadd_rn(sQ[c], sw[m])));
+        const double S = __dadd_rn(Pr, __dadd_rn(Rc, __dadd_rn(Qc, sw[m])));
         if (S < sx) lo = m + 1;
         else hi = m;
       }
@@ -324,7 +366,8 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
   if ((uintptr_t)w & 7) return DRS_ERR_ALIGN;
   const int ntt = (int)cdiv(Mf, TS_TABLE);
   const int ntu = (int)cdiv(Nf + 1, TS_UNIF);
-  const size_t smem = (size_t)(TS_TABLE + THREADS + ((Nf + 1 + 15) & ~(int64_t)15)) * 8;
+  // su holds N_f + 1 doubles and, first, the Philox words of a one-tile draw
+  const size_t smem = (size_t)(TS_TABLE + THREADS + ((Nf + 1 + 8 + 15) & ~(int64_t)15)) * 8;
   if (ntt > MAX_TT || ntu > MAX_UT || smem > (size_t)(227 * 1024 - 1024)) return DRS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
