@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
         if (e0 + i < ne) su[e0 + i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
       __syncthreads();  // fs reuse
     }
-    if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
+    block_min_u64(&s_min, mn);
     double Pu[MAX_UT];
     double total = 0.0;
 #pragma unroll

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   sc[0] = z[0];
 #pragma unroll
   for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
-  atomicMin(&s_min, mn);
+  block_min_u64(&s_min, mn);
   double Q, R;
   const double A = block_fold(sc[K_UNIF - 1], fs, Q, R);
   STAMP(2);

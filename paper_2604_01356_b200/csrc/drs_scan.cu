@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
     for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) ws.incl[t] = sa[t - c0];
     __syncthreads();
   }
-  if (mode == 1) atomicMin(&s_min, mn);
+  if (mode == 1) block_min_u64(&s_min, mn);
   __syncthreads();
   if (threadIdx.x == 0) {
     double C = 0.0;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   sc[0] = z[0];
 #pragma unroll
   for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
-  if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
+  block_min_u64(&s_min, mn);
   double Q, R;
   const double A = block_fold(sc[K_UNIF - 1], fs, Q, R);  // contains __syncthreads
   if (threadIdx.x == 0) {

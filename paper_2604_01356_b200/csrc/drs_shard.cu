@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_tile_totals(PhiloxSpacings src
   double sc = z[0];
 #pragma unroll
   for (int i = 1; i < K_UNIF; ++i) sc = __dadd_rn(sc, z[i]);
-  if (mn != 0x7FF0000000000000ULL) atomicMin(&s_min, mn);
+  block_min_u64(&s_min, mn);
   double Q, R;
   const double A = block_fold(sc, fs, Q, R);
   if (threadIdx.x == 0) {
