@@ -178,10 +178,13 @@ int dr_lower_bound_range(const double *W, int64_t lo, int64_t hi, double x, int6
 /* Batched independent filters (config 4; the reference's per-filter loop
  * over build_weight_table + dac_sampler): w[B][Mf] raw weights, keys[B][3]
  * (k0, k1, draw offset per filter) -> out[B][Nf]; U[B][Nf] and W[B][Mf]
- * are written when non-NULL.  With advance != 0 each filter's draw offset
- * is moved forward by Nf + 1 on the device (graph-replayable).  Persistent
- * CTAs, weights staged in shared memory by TMA with L2 prefetch ahead.
- * status gets the OR over filters.  Needs Mf*8 + (Nf+1)*8 + tables <= ~220 KB. */
+ * are written when non-NULL (U is stream-ordered scratch otherwise).  With
+ * advance != 0 each filter's draw offset is moved forward by Nf + 1 on the
+ * device (graph-replayable).  Two launches: the uniforms of every filter,
+ * then one thread-block cluster per filter (one CTA per 8448-weight tile,
+ * tile staged in shared memory by TMA, tile totals exchanged through
+ * distributed shared memory).  status gets the OR over filters.  Needs
+ * Mf <= 8 x 8448 and Nf + 1 <= 8 x 512. */
 int dr_resample_batched(const double *w, int64_t B, int64_t Mf, int64_t Nf, uint64_t *keys,
                         int32_t advance, double *W, double *U, int64_t *out, int32_t *status,
                         void *stream);

@@ -2,17 +2,18 @@
 //
 // The reference resamples a bank of filters with a Python loop of
 // build_weight_table (cdf.py:59-89) + dac_sampler (samplers.py:262-266) per
-// filter.  Here one thread-block CLUSTER owns one filter, one CTA per table
-// tile of the chained scan (THREADS x K_TABLE = 8448 weights; M_f = 16384 is
-// a 2-CTA cluster):
+// filter.  Here two launches serve the whole bank:
 //
+//   k_batched_uniforms  one small CTA per filter draws the N_f + 1 Philox
+//     spacings (each Philox block once), folds them with the association of
+//     dr_sorted_uniforms, normalises, repairs collapses and writes U[f]; small
+//     CTAs (8+ per SM) keep this compute-bound step wide;
+//   k_resample_batched  one thread-block CLUSTER per filter, one CTA per table
+//     tile of the chained scan (THREADS x K_TABLE = 8448 weights; M_f = 16384
+//     is a 2-CTA cluster):
 //   * CTA r stages its tile of w_f in shared memory with one TMA bulk copy
 //     (~66 KB, so three CTAs share an SM and one CTA's copy overlaps the
-//     others' compute);
-//   * while the copy is in flight it generates and scans the N_f + 1 Philox
-//     spacings (they do not depend on w; every CTA of the cluster derives the
-//     same U, exactly as dr_sorted_uniforms does; with N_f + 1 <= 512 each
-//     Philox block is computed once, by one thread);
+//     others' compute) and U[f] with a second one;
 //   * ONE sweep over the tile: each lane folds its K_TABLE-element chunk
 //     serially (validating from the high words in the integer pipe), writes
 //     the chunk-local prefix s2 in place, and the CTA folds lane and warp
@@ -22,11 +23,13 @@
 //     (st.shared::cluster + one cluster barrier); every CTA then folds the
 //     tile prefixes P_r and the filter total T in tile order;
 //   * CTA r answers exactly the draws u with W_end(r-1) < u <= W_end(r),
-//     W_end(r) = min(P_{r+1} / T, 1) being W at the tile's last entry, by
-//     bisection over its tile whose probes form
-//     W_j = min((P_r + (R + (Q + s2_j))) / T, 1) on the fly (~13 divisions
-//     per draw instead of one per weight; all of W only on request).
-// Global traffic per filter: w_f once, U and the indices (+ W on request).
+//     W_end(r) = min(P_{r+1} / T, 1) being W at the tile's last entry, by a
+//     bisection over its lane-chunk ends and then inside the chunk, whose
+//     probes form W_j = min((P_r + (R + (Q + s2_j))) / T, 1) on the fly
+//     (a few divisions per draw instead of one per weight; all of W only on
+//     request).
+// Global traffic per filter: w_f once, U twice (written, read), the indices
+// (+ W on request).
 // The (k0, k1, offset) stream keys are read on the device and, with
 // `advance`, moved forward by N_f + 1 there (graph-replayable).  Filters
 // shard across GPUs with no collective.
@@ -92,54 +95,29 @@ struct BatchedArgs {
   int advance;     // move keys[f][2] forward by Nf + 1 on the device
   double* Wout;    // optional [B][Mf]
   double* Uout;    // optional [B][Nf]
+  const double* Uin;  // [B][Nf] from k_batched_uniforms
   int64_t* out;    // [B][Nf]
   int32_t* status;
   int ntt, ntu;
 };
 
-__global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
-  extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bar;
-  __shared__ FoldSmem fs;         // fold of a uniform tile, then of the table tile
-  __shared__ double s_R[WARPS];   // warp bases R of the table tile
-  __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
+// Sorted uniforms of every filter: one CTA per filter draws its N_f + 1
+// spacings (each Philox block once when they fit one tile), folds them with
+// the association of dr_sorted_uniforms, normalises, repairs collapses and
+// writes U[f] -- all filters in one wide launch of small CTAs (8 or more per
+// SM), so the cluster kernel below only reads 8 N_f bytes per filter.
+__global__ void __launch_bounds__(THREADS) k_batched_uniforms(const __grid_constant__ BatchedArgs a,
+                                                              double* __restrict__ U) {
+  extern __shared__ __align__(128) double su[];  // [ne + 8]: Philox words, inner sums, then U
+  __shared__ FoldSmem fs;
   __shared__ double s_Au[MAX_UT];
   __shared__ unsigned long long s_min;
-  __shared__ int s_bad;
-  __shared__ int s_range[2];
-  __shared__ double s_cend[THREADS];  // S at each lane chunk's last entry
-  const int64_t Mf = a.Mf, Nf = a.Nf, ne = Nf + 1;
-  const int r = (int)cluster_rank();
-  const int64_t f = blockIdx.x / a.ntt;
-  const int64_t j0 = (int64_t)r * TS_TABLE;  // first weight of this tile
-  const int len = (int)((Mf - j0) < TS_TABLE ? (Mf - j0) : TS_TABLE);
-  double* sw = sm;             // [TS_TABLE] raw w, then chunk-local prefixes s2
-  double* sQ = sw + TS_TABLE;  // [THREADS] lane-chunk bases Q
-  double* su = sQ + THREADS;   // [ne] inner sums, then U
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const double* wt = a.w + f * Mf + j0;
-  const bool tma = ((((uintptr_t)wt) | ((uintptr_t)len * 8)) & 15) == 0;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    if (tma) {
-      mbar_expect_tx(&bar, (uint32_t)len * 8u);
-      bulk_g2s(sw, wt, (uint32_t)len * 8u, &bar);
-    }
-    s_min = 0x7FF0000000000000ULL;
-    s_bad = 0;
-  }
-  if (!tma)
-    for (int i = threadIdx.x; i < len; i += THREADS) sw[i] = wt[i];
-  for (int i = len + threadIdx.x; i < TS_TABLE; i += THREADS) sw[i] = 0.0;  // tile padding
+  const int64_t Nf = a.Nf, ne = Nf + 1;
+  const int64_t f = blockIdx.x;
+  const int r = 0;
   const uint64_t k0 = a.keys[3 * f], k1 = a.keys[3 * f + 1], off = a.keys[3 * f + 2];
+  if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
   __syncthreads();
-  STAMP(0);
-  // first half of a split cluster barrier: peers may store into this CTA's
-  // shared memory only once every CTA of the cluster is running
-  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-
-  // ---- 1. spacings and sorted uniforms, while the weights are in flight
   if (Nf > 0) {
     unsigned long long mn = 0x7FF0000000000000ULL;
     for (int t = 0; t < a.ntu; ++t) {
@@ -215,6 +193,63 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
     uniform_repair(su, Nf, s_min, total, r, a.status);
   }
 
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < Nf; i += THREADS) U[f * Nf + i] = su[i];
+  if (threadIdx.x == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every thread has read it
+}
+
+__global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar, baru;
+  __shared__ FoldSmem fs;         // fold of the table tile
+  __shared__ double s_R[WARPS];   // warp bases R of the table tile
+  __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
+  __shared__ int s_bad;
+  __shared__ int s_range[2];
+  __shared__ double s_cend[THREADS];  // S at each lane chunk's last entry
+  const int64_t Mf = a.Mf, Nf = a.Nf, ne = Nf + 1;
+  const int r = (int)cluster_rank();
+  const int64_t f = blockIdx.x / a.ntt;
+  const int64_t j0 = (int64_t)r * TS_TABLE;  // first weight of this tile
+  const int len = (int)((Mf - j0) < TS_TABLE ? (Mf - j0) : TS_TABLE);
+  double* sw = sm;             // [TS_TABLE] raw w, then chunk-local prefixes s2
+  double* sQ = sw + TS_TABLE;  // [THREADS] lane-chunk bases Q
+  double* su = sQ + THREADS;   // [ne] inner sums, then U
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const double* wt = a.w + f * Mf + j0;
+  const bool tma = ((((uintptr_t)wt) | ((uintptr_t)len * 8)) & 15) == 0;
+
+  const double* ut = a.Uin + f * Nf;
+  const bool tmau = Nf > 0 && ((((uintptr_t)ut) | ((uintptr_t)Nf * 8)) & 15) == 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init(&baru, 1);
+    if (tma) {
+      mbar_expect_tx(&bar, (uint32_t)len * 8u);
+      bulk_g2s(sw, wt, (uint32_t)len * 8u, &bar);
+    }
+    if (tmau) {
+      mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
+      bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
+    }
+    s_bad = 0;
+  }
+  if (!tma)
+    for (int i = threadIdx.x; i < len; i += THREADS) sw[i] = wt[i];
+  for (int i = len + threadIdx.x; i < TS_TABLE; i += THREADS) sw[i] = 0.0;  // tile padding
+  __syncthreads();
+  STAMP(0);
+  // first half of a split cluster barrier: peers may store into this CTA's
+  // shared memory only once every CTA of the cluster is running
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+
+  // ---- 1. this filter's sorted uniforms (k_batched_uniforms), with the weights
+  if (Nf > 0) {
+    if (!tmau)
+      for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = a.Uin[f * Nf + i];
+    if (tmau) mbar_wait(&baru, 0);
+  }
+
   // ---- 2. the table sweep over this CTA's tile
   STAMP(1);
   if (tma) mbar_wait(&bar, 0);
@@ -273,7 +308,6 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
     if (r == 0) {
       if (T == 0.0) st |= DRS_ST_DEGENERATE;
       if (!(T < dinf())) st |= DRS_ST_ACCUM_OVERFLOW;
-      if (a.advance && Nf > 0) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every CTA has read it
     }
     if (st) atomicOr(a.status, st);
   }
@@ -335,7 +369,6 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
         else hi = m;
       }
       a.out[f * Nf + i] = j0 + lo;
-      if (a.Uout) a.Uout[f * Nf + i] = x;
     }
   }
   STAMP(5);
@@ -377,7 +410,21 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
     cudaFuncSetAttribute(k_resample_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     c_smem = smem;
   }
-  BatchedArgs a{w, B, Mf, Nf, keys, advance, W, U, out, status, ntt, ntu};
+  // U: the caller's buffer, else stream-ordered scratch (graph-capturable)
+  double* Ub = U;
+  if (!Ub && Nf > 0 && cudaMallocAsync((void**)&Ub, sizeof(double) * (size_t)(B * Nf), st) != cudaSuccess)
+    return DRS_ERR_LAUNCH;
+  BatchedArgs a{w, B, Mf, Nf, keys, advance, W, Ub, Ub, out, status, ntt, ntu};
+  if (Nf > 0) {
+    const size_t usmem = (size_t)((Nf + 1 + 8 + 15) & ~(int64_t)15) * 8;
+    static size_t c_usmem = 0;
+    if (c_usmem < usmem) {
+      cudaFuncSetAttribute(k_batched_uniforms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
+      c_usmem = usmem;
+    }
+    k_batched_uniforms<<<(unsigned)B, THREADS, usmem, st>>>(a, Ub);
+    if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(B * ntt));
   cfg.blockDim = dim3(THREADS);
@@ -391,5 +438,6 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_resample_batched, a);
+  if (!U && Nf > 0 && cudaFreeAsync(Ub, st) != cudaSuccess) return DRS_ERR_LAUNCH;
   return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
