@@ -108,6 +108,7 @@ struct BatchedArgs {
 // SM), so the cluster kernel below only reads 8 N_f bytes per filter.
 __global__ void __launch_bounds__(THREADS) k_batched_uniforms(const __grid_constant__ BatchedArgs a,
                                                               double* __restrict__ U) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the cluster kernel may start its weight copies
   extern __shared__ __align__(128) double su[];  // [ne + 8]: Philox words, inner sums, then U
   __shared__ FoldSmem fs;
   __shared__ double s_Au[MAX_UT];
@@ -198,6 +199,80 @@ __global__ void __launch_bounds__(THREADS) k_batched_uniforms(const __grid_const
   if (threadIdx.x == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every thread has read it
 }
 
+// N_f + 1 <= 512 (one uniform tile): one CTA of nw = ceil((N_f + 1) / 64)
+// warps per filter -- the tile's lanes past N_f + 1 hold zeros, so folding
+// only the first nw warps gives block_fold's bits (x + 0.0 == x) -- with each
+// Philox block computed once, by one thread.
+__global__ void __launch_bounds__(THREADS) k_batched_uniforms1(const __grid_constant__ BatchedArgs a,
+                                                               double* __restrict__ U) {
+  asm volatile("griddepcontrol.launch_dependents;");  // the cluster kernel may start its weight copies
+  __shared__ double su[TS_UNIF + 8];  // Philox words, then U
+  __shared__ double s_tau[WARPS * (LANES + 1)];
+  __shared__ double s_G[WARPS];
+  __shared__ unsigned long long s_min;
+  const int64_t Nf = a.Nf, ne = Nf + 1;
+  const int64_t f = blockIdx.x;
+  const int nw = (int)(blockDim.x >> 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t k0 = a.keys[3 * f], k1 = a.keys[3 * f + 1], off = a.keys[3 * f + 2];
+  uint64_t* words = reinterpret_cast<uint64_t*>(su);
+  const uint64_t b0 = off >> 2;
+  const int nblk = (int)(((off + (uint64_t)ne - 1) >> 2) - b0 + 1);
+  if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
+  for (int blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
+    const U64x4 v = philox_block(k0, k1, b0 + (uint64_t)blk);
+    words[4 * blk + 0] = v.w0; words[4 * blk + 1] = v.w1;
+    words[4 * blk + 2] = v.w2; words[4 * blk + 3] = v.w3;
+  }
+  __syncthreads();
+  const int64_t e0 = (int64_t)threadIdx.x * K_UNIF;
+  const int a0 = (int)(off & 3);
+  double z[K_UNIF];
+  unsigned long long mn = 0x7FF0000000000000ULL;
+#pragma unroll
+  for (int i = 0; i < K_UNIF; ++i) {
+    z[i] = 0.0;
+    if (e0 + i < ne) {
+      z[i] = neglog(u01(words[a0 + e0 + i]));
+      mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
+    }
+  }
+  block_min_u64(&s_min, mn);
+  double sc[K_UNIF];
+  sc[0] = z[0];
+#pragma unroll
+  for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
+  // block_fold over the nw warps
+  s_tau[warp * (LANES + 1) + lane] = sc[K_UNIF - 1];
+  __syncthreads();
+  if ((int)threadIdx.x < nw) {
+    double* row = s_tau + threadIdx.x * (LANES + 1);
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < LANES; ++l) {
+      const double v = row[l];
+      row[l] = acc;
+      acc = __dadd_rn(acc, v);
+    }
+    s_G[threadIdx.x] = acc;
+  }
+  __syncthreads();
+  double R = 0.0, A = 0.0;
+  for (int w = 0; w < nw; ++w) {
+    if (w == warp) R = A;
+    A = __dadd_rn(A, s_G[w]);
+  }
+  const double Q = s_tau[warp * (LANES + 1) + lane];
+#pragma unroll
+  for (int i = 0; i < K_UNIF; ++i)
+    if (e0 + i < Nf) su[e0 + i] = __ddiv_rn(__dadd_rn(R, __dadd_rn(Q, sc[i])), A);
+  __syncthreads();
+  uniform_repair(su, Nf, s_min, A, 0, a.status);
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < Nf; i += blockDim.x) U[f * Nf + i] = su[i];
+  if (threadIdx.x == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every thread has read it
+}
+
 __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar, baru;
@@ -223,14 +298,9 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   const bool tmau = Nf > 0 && ((((uintptr_t)ut) | ((uintptr_t)Nf * 8)) & 15) == 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
-    mbar_init(&baru, 1);
     if (tma) {
       mbar_expect_tx(&bar, (uint32_t)len * 8u);
       bulk_g2s(sw, wt, (uint32_t)len * 8u, &bar);
-    }
-    if (tmau) {
-      mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
-      bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
     }
     s_bad = 0;
   }
@@ -243,11 +313,23 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   // shared memory only once every CTA of the cluster is running
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
-  // ---- 1. this filter's sorted uniforms (k_batched_uniforms), with the weights
+  // ---- 1. this filter's sorted uniforms.  The launch may overlap the tail of
+  // k_batched_uniforms (programmatic dependent launch): the weight copy above
+  // is already in flight; U is read only after the uniforms grid completed.
   if (Nf > 0) {
-    if (!tmau)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tmau) {
+      if (threadIdx.x == 0) {
+        mbar_init(&baru, 1);
+        mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
+        bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
+      }
+      __syncthreads();
+      mbar_wait(&baru, 0);
+    } else {
       for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = a.Uin[f * Nf + i];
-    if (tmau) mbar_wait(&baru, 0);
+      __syncthreads();
+    }
   }
 
   // ---- 2. the table sweep over this CTA's tile
@@ -422,7 +504,12 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
       cudaFuncSetAttribute(k_batched_uniforms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
       c_usmem = usmem;
     }
-    k_batched_uniforms<<<(unsigned)B, THREADS, usmem, st>>>(a, Ub);
+    if (ntu == 1) {
+      const int nw = (int)cdiv(cdiv(Nf + 1, K_UNIF), LANES);
+      k_batched_uniforms1<<<(unsigned)B, (unsigned)(nw * LANES), 0, st>>>(a, Ub);
+    } else {
+      k_batched_uniforms<<<(unsigned)B, THREADS, usmem, st>>>(a, Ub);
+    }
     if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
   }
   cudaLaunchConfig_t cfg = {};
@@ -430,13 +517,15 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)ntt;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the uniforms' tail
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = Nf > 0 ? 2 : 1;
   const cudaError_t e = cudaLaunchKernelEx(&cfg, k_resample_batched, a);
   if (!U && Nf > 0 && cudaFreeAsync(Ub, st) != cudaSuccess) return DRS_ERR_LAUNCH;
   return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
