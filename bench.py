@@ -171,7 +171,7 @@ def run_drs(args, rank, world, local_rank):
             # stream positions live on the device and advance there
             return drs.resample_batched(w, Nf, bstreams, return_uniforms=True, check=False, device=True)
 
-        launches_per_step = 1
+        launches_per_step = 2  # the bank's uniforms, then one cluster per filter
         kernel_step = step
         w_pinned = torch.from_numpy(w_host).pin_memory()
         # end to end: pinned host weights in, host indices out (status read included)
