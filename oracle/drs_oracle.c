@@ -301,13 +301,45 @@ int drs_ref_sorted_uniforms_from(const double *raw, int64_t n, double *U) {
 /* every FANOUT^k-block of W, each level padded with +inf to a multiple of  */
 /* FANOUT; levels stop once a level has <= FANOUT entries.                  */
 /* ------------------------------------------------------------------------ */
+/* After the levels comes the top guide (Chen & Asau's guide table over one */
+/* level): kt = the lowest level with <= 16384 entries, B = 2^tshift the    */
+/* least power of two >= n_kt / 2 (and >= 16), Gt[b] = lower bound of b / B */
+/* among level kt's entries (clamped to n_kt - 1) for b = 0 .. B+1, int32   */
+/* packed two per double, zero-padded to a multiple of FANOUT doubles.      */
+/* Mirrors make_index_desc / k_build_top_guide.                             */
+static void ref_top_guide(int64_t M, int *kt, int64_t *nkt, int *tshift, int64_t *tdoubles) {
+  int64_t n = M;
+  int L = 0;
+  *kt = 0;
+  *nkt = 0;
+  while (n > DRS_REF_FANOUT) {
+    n = (n + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT;
+    ++L;
+    if (!*kt && n <= 16384) {
+      *kt = L;
+      *nkt = n;
+    }
+  }
+  *tshift = 0;
+  *tdoubles = 0;
+  if (!*kt) return;
+  int sh = 0;
+  while (((int64_t)2 << sh) < *nkt) ++sh;
+  *tshift = sh < 4 ? 4 : sh;
+  const int64_t n32 = ((int64_t)1 << *tshift) + 2;
+  *tdoubles = ((n32 + 1) / 2 + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT * DRS_REF_FANOUT;
+}
+
 int64_t drs_ref_index_entries(int64_t M) {
   int64_t total = 0, n = M;
   while (n > DRS_REF_FANOUT) {
     n = (n + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT;
     total += (n + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT * DRS_REF_FANOUT;
   }
-  return total;
+  int kt, tshift;
+  int64_t nkt, td;
+  ref_top_guide(M, &kt, &nkt, &tshift, &td);
+  return total + td;
 }
 
 void drs_ref_build_index(const double *W, int64_t M, double *idx) {
@@ -327,6 +359,33 @@ void drs_ref_build_index(const double *W, int64_t M, double *idx) {
       }
     }
     off += padded;
+  }
+  int kt, tshift;
+  int64_t nkt, td;
+  ref_top_guide(M, &kt, &nkt, &tshift, &td);
+  if (!kt) return;
+  /* level kt starts where the levels below it end */
+  int64_t koff = 0, m = M;
+  for (int k = 1; k < kt; ++k) {
+    m = (m + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT;
+    koff += (m + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT * DRS_REF_FANOUT;
+  }
+  const double *Lk = idx + koff;
+  int32_t *G = (int32_t *)(idx + off);
+  const int64_t B = (int64_t)1 << tshift;
+  for (int64_t b = 0; b < 2 * td; ++b) {
+    if (b > B + 1) {
+      G[b] = 0;
+      continue;
+    }
+    const double x = (double)b / (double)B;
+    int64_t lo = 0, hi = nkt - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (Lk[mid] < x) lo = mid + 1;
+      else hi = mid;
+    }
+    G[b] = (int32_t)lo;
   }
 }
 

@@ -52,11 +52,16 @@ struct SmemLevels {
   int k_smem;       // levels k >= k_smem are staged in shared memory (k_smem > levels: none)
   int64_t base;     // idx offset of level k_smem
   int64_t count;    // doubles staged
+  int tg;           // the top guide is staged too (k_smem == kt): the search enters at level kt
 };
 
 SmemLevels plan_smem_levels(const IndexDesc& d, int64_t cap = SIDX_CAP) {
-  SmemLevels s{d.levels + 1, 0, 0};
+  SmemLevels s{d.levels + 1, 0, 0, 0};
   if (d.levels == 0) return s;
+  if (d.kt) {  // level kt, the levels above it and the top guide: one contiguous range
+    const int64_t need = d.toff + tg_doubles(d) - d.off[d.kt];
+    if (need <= cap) return SmemLevels{d.kt, d.off[d.kt], need, 1};
+  }
   const int64_t end = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
   for (int k = d.levels; k >= 1; --k) {
     if (end - d.off[k] > cap) break;
@@ -86,7 +91,28 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
   int64_t b[K_UNIF];
 #pragma unroll
   for (int q = 0; q < K_UNIF; ++q) b[q] = 0;
-  for (int k = d.levels; k >= 1; --k) {
+  int ktop = d.levels;
+  if (sl.tg) {
+    // the top guide: the level-kt node from one bucket, [Gt[b], Gt[b+1]]
+    // narrowed by a bisection over level kt (in shared memory; mostly empty)
+    const int32_t* Gt = reinterpret_cast<const int32_t*>(sidx + (d.toff - sl.base));
+    const double* Lk = sidx + (d.off[d.kt] - sl.base);
+    const int64_t B = (int64_t)1 << d.tshift;
+#pragma unroll
+    for (int q = 0; q < K_UNIF; ++q) {
+      const double xb = x[q] * (double)B;
+      const int64_t bk = (xb >= (double)B) ? B : ((xb > 0.0) ? (int64_t)xb : 0);  // NaN -> 0
+      int lo = Gt[bk], hi = Gt[bk + 1];
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (Lk[m] < x[q]) lo = m + 1;
+        else hi = m;
+      }
+      b[q] = lo;
+    }
+    ktop = d.kt - 1;
+  }
+  for (int k = ktop; k >= 1; --k) {
     int c[K_UNIF];
     if (k >= sl.k_smem) {
       const double* base = sidx + (d.off[k] - sl.base);

@@ -284,13 +284,44 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
   return launch_rc();
 }
 
+// the top guide (drs_common.cuh) from the finished level kt: one thread per
+// bucket, a bisection among level kt's entries (L2-resident, <= 16384 of them);
+// the storage tail past bucket B + 1 is zeroed
+__global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ idx, IndexDesc d) {
+  int32_t* G = reinterpret_cast<int32_t*>(idx + d.toff);
+  const int64_t cap = 2 * tg_doubles(d), nb = ((int64_t)1 << d.tshift) + 2;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= cap) return;
+  if (b >= nb) {
+    G[b] = 0;
+    return;
+  }
+  const double x = (double)b / (double)((int64_t)1 << d.tshift);  // exact
+  const double* L = idx + d.off[d.kt];
+  int64_t lo = 0, hi = d.n[d.kt] - 1;
+  while (lo < hi) {
+    const int64_t m = (lo + hi) >> 1;
+    if (L[m] < x) lo = m + 1;
+    else hi = m;
+  }
+  G[b] = (int32_t)lo;
+}
+
+int launch_top_guide(int64_t M, double* idx, cudaStream_t st) {
+  const IndexDesc d = make_index_desc(M);
+  if (!d.kt) return DRS_OK;
+  k_build_top_guide<<<(unsigned)cdiv(2 * tg_doubles(d), 256), 256, 0, st>>>(idx, d);
+  return launch_rc();
+}
+
 int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
   if (d.levels == 0) return DRS_OK;
   if (!idx) return DRS_ERR_ARG;
   const int64_t total = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
   k_build_index<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(W, M, idx, d, total);
-  return launch_rc();
+  if (launch_rc()) return DRS_ERR_LAUNCH;
+  return launch_top_guide(M, idx, st);
 }
 
 int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,

@@ -485,6 +485,8 @@ __global__ void k_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t k,
 }
 
 // --------------------------------------------------------------- host ----
+int launch_top_guide(int64_t M, double* idx, cudaStream_t st);  // drs_match.cu
+
 IndexDesc make_index_desc(int64_t M) {
   IndexDesc d{};
   d.n[0] = M;
@@ -499,6 +501,18 @@ IndexDesc make_index_desc(int64_t M) {
     off += cdiv(n, FANOUT) * FANOUT;
   }
   d.levels = L;
+  d.kt = 0;
+  d.tshift = 0;
+  d.toff = 0;
+  if (L > 0) {
+    int k = 1;
+    while (d.n[k] > DRS_TG_ENTRIES) ++k;  // n[L] <= FANOUT, so k <= L
+    int sh = 0;
+    while (((int64_t)2 << sh) < d.n[k]) ++sh;  // 2^(sh+1) >= n[kt]
+    d.kt = k;
+    d.tshift = sh < 4 ? 4 : sh;
+    d.toff = off;
+  }
   return d;
 }
 
@@ -521,7 +535,7 @@ static void set_attrs() {
 int64_t index_entries(int64_t M) {
   const IndexDesc d = make_index_desc(M);
   if (d.levels == 0) return 0;
-  return d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
+  return d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT + tg_doubles(d);
 }
 
 int64_t ws_capacity_tiles(size_t ws_bytes) { return ws_tile_capacity(ws_bytes); }
@@ -626,7 +640,8 @@ int dr_build_table(const double* w, int64_t M, double* W, double* idx, int32_t* 
   k_table_pass1<false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, s, nullptr);
   launch_chain(s, nt, 0, status, nullptr, st);
   k_table_pass2<false, false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, nt, s, W, idx, d, status, nullptr);
-  return launch_rc();
+  if (launch_rc()) return DRS_ERR_LAUNCH;
+  return launch_top_guide(M, idx, st);
 }
 
 int dr_build_table_log(const double* logw, int64_t M, double* W, double* idx, int32_t* status, void* ws,
@@ -648,7 +663,8 @@ int dr_build_table_log(const double* logw, int64_t M, double* W, double* idx, in
   k_table_pass1<true><<<(unsigned)nt, THREADS, smem, st>>>(logw, M, s, W);  // w -> W
   launch_chain(s, nt, 0, status, nullptr, st);
   k_table_pass2<false, false><<<(unsigned)nt, THREADS, smem, st>>>(W, M, nt, s, W, idx, d, status, nullptr);
-  return launch_rc();
+  if (launch_rc()) return DRS_ERR_LAUNCH;
+  return launch_top_guide(M, idx, st);
 }
 
 int dr_shard_scan(const double* w_shard, int64_t Mg, double* S, double* Tg, int32_t* status,
