@@ -51,3 +51,15 @@ for name, a in (("device out", dev), ("pinned out", host)):
 clock("public dac_sampler host", lambda: drs.dac_sampler(table, N, drs.RngStream(5)), 300)
 st = drs.RngStream(5)
 clock("public dac_sampler host (one stream)", lambda: drs.dac_sampler(table, N, st), 300)
+
+# fixed costs: a trivial torch kernel + stream sync, and a sync with nothing queued
+x = torch.zeros(1, device="cuda")
+clock("torch tiny kernel + synchronize", lambda: (x.add_(1), L.dr_stream_synchronize(s)), 1000)
+clock("dr_stream_synchronize, idle stream", lambda: L.dr_stream_synchronize(s), 1000)
+ev = torch.cuda.Event()
+def ev_spin():
+    L.dr_sample_dac(*dev)
+    ev.record()
+    while not ev.query():
+        pass
+clock("launch + event query spin, device out", ev_spin, 300)
