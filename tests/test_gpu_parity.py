@@ -281,7 +281,11 @@ def test_batched_bit_exact_vs_oracle(drs, orc):
 
 
 @pytest.mark.parametrize("B,Mf,Nf", [(300, 16384, 256), (333, 16383, 257), (7, 12000, 3000), (5, 1, 4),
-                                     (200, 33, 1), (4, 8449, 1023), (3, 25000, 0)])
+                                     (200, 33, 1), (4, 8449, 1023), (3, 25000, 0),
+                                     # row and tile edges, one and two tiles, many filters per SM
+                                     (157, 16896, 511), (150, 2, 1), (149, 34, 5), (200, 1056, 64),
+                                     (200, 1058, 63), (211, 8448, 100), (211, 8450, 300), (90, 9504, 200),
+                                     (50, 4096, 0), (400, 16000, 130)])
 def test_batched_shapes_vs_oracle(drs, orc, B, Mf, Nf):
     """Tile edges, odd M_f (no TMA path), several table / uniform tiles, more
     filters than resident CTAs, N_f = 0; bit-exact against the oracle."""
@@ -297,6 +301,35 @@ def test_batched_shapes_vs_oracle(drs, orc, B, Mf, Nf):
     np.testing.assert_array_equal(res[1], Uo)
     np.testing.assert_array_equal(res[0], eo)
     assert all(s.position == (Nf + 1 if Nf else 0) for s in streams)
+
+
+@pytest.mark.parametrize("case", ["heavy_chunk", "zero_rows", "spike_first", "no_tables"])
+def test_batched_mass_layouts(drs, orc, case):
+    """Many draws in one chunk, whole zero rows, mass in the first or last
+    entry, and the index-only call (no W / U outputs), over more filters than
+    resident CTAs."""
+    rng = np.random.default_rng(["heavy_chunk", "zero_rows", "spike_first", "no_tables"].index(case))
+    B, Mf, Nf = 700, 16384, 256
+    w = np.exp(rng.standard_normal((B, Mf)))
+    if case == "heavy_chunk":
+        w[:, 5000] = 1e6
+        w[::2, 16383] = 1e6
+    elif case == "zero_rows":
+        w[:, 1056:3168] = 0.0
+        w[:, :40] = 0.0
+        w[:, 16000:] = 0.0
+    elif case == "spike_first":
+        w[:, 0] = 1e9
+    streams = [drs.RngStream(7, (b,)) for b in range(B)]
+    keys = np.array([[s.key[0], s.key[1], s.position] for s in streams], dtype=np.uint64)
+    eo, Uo, Wo, st = orc.resample_batched(w, Nf, keys)
+    if case == "no_tables":
+        out = drs.resample_batched(w, Nf, streams)
+    else:
+        out, U, W = drs.resample_batched(w, Nf, streams, return_uniforms=True, return_tables=True)
+        np.testing.assert_array_equal(W, Wo)
+        np.testing.assert_array_equal(U, Uo)
+    np.testing.assert_array_equal(out, eo)
 
 
 def test_batched_device_streams_advance(drs, orc):
