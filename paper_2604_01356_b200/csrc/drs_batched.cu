@@ -199,78 +199,128 @@ __global__ void __launch_bounds__(THREADS) k_batched_uniforms(const __grid_const
   if (threadIdx.x == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every thread has read it
 }
 
-// N_f + 1 <= 512 (one uniform tile): one CTA of nw = ceil((N_f + 1) / 64)
-// warps per filter -- the tile's lanes past N_f + 1 hold zeros, so folding
-// only the first nw warps gives block_fold's bits (x + 0.0 == x) -- with each
-// Philox block computed once, by one thread.
-__global__ void __launch_bounds__(THREADS) k_batched_uniforms1(const __grid_constant__ BatchedArgs a,
-                                                               double* __restrict__ U) {
+// N_f + 1 <= 512 (one uniform tile): ONE WARP per filter, eight filters per
+// CTA, no CTA barrier.  Lane l holds the two spacings 64 w + 2 l, + 1 of every
+// spacing row w < nw = ceil((N_f + 1) / 64) -- the lane chunks of
+// dr_sorted_uniforms' tile (rows past nw hold zeros, so folding only nw rows
+// gives the tile fold's bits: x + 0.0 == x).  The filter's Philox blocks are
+// computed once each (lane b takes blocks b, b + 32, ...) into the warp's
+// shared buffer; lane w folds row w's 32 chunk totals serially in place
+// (the row bases Q), every lane folds the row totals (R, A); U is divided in
+// registers and stored 16 bytes per lane.  The exactness check / repair of
+// randkit.py:95-116 runs on lane 0 when the spacing minimum asks for it.
+constexpr int UW_FILTERS = 4;                 // warps (filters) per CTA
+constexpr int UW_BUF = TS_UNIF + 8;           // doubles per warp: Philox words, then row totals, then U
+template <int NW>  // spacing rows = ceil((N_f + 1) / 64), unrolled without guards
+__global__ void __launch_bounds__(UW_FILTERS * LANES, 6) k_batched_uniforms_warp(const __grid_constant__ BatchedArgs a,
+                                                                                double* __restrict__ U) {
   asm volatile("griddepcontrol.launch_dependents;");  // the cluster kernel may start its weight copies
-  __shared__ double su[TS_UNIF + 8];  // Philox words, then U
-  __shared__ double s_tau[WARPS * (LANES + 1)];
-  __shared__ double s_G[WARPS];
-  __shared__ unsigned long long s_min;
-  const int64_t Nf = a.Nf, ne = Nf + 1;
-  const int64_t f = blockIdx.x;
-  const int nw = (int)(blockDim.x >> 5);
+  __shared__ __align__(16) double sbuf[UW_FILTERS][UW_BUF];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t f = (int64_t)blockIdx.x * UW_FILTERS + warp;
+  if (f >= a.B) return;
+  const int64_t Nf = a.Nf, ne = Nf + 1;
+  constexpr int nw = NW;
+  double* buf = sbuf[warp];
+  uint64_t* words = reinterpret_cast<uint64_t*>(buf);
   const uint64_t k0 = a.keys[3 * f], k1 = a.keys[3 * f + 1], off = a.keys[3 * f + 2];
-  uint64_t* words = reinterpret_cast<uint64_t*>(su);
   const uint64_t b0 = off >> 2;
-  const int nblk = (int)(((off + (uint64_t)ne - 1) >> 2) - b0 + 1);
-  if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
-  for (int blk = threadIdx.x; blk < nblk; blk += blockDim.x) {
+  const int nblk = (int)(((off + (uint64_t)Nf) >> 2) - b0 + 1);
+  for (int blk = lane; blk < nblk; blk += 2 * LANES) {  // two blocks per lane in flight
+    const int blk2 = blk + LANES;
     const U64x4 v = philox_block(k0, k1, b0 + (uint64_t)blk);
+    const U64x4 v2 = philox_block(k0, k1, b0 + (uint64_t)blk2);
     words[4 * blk + 0] = v.w0; words[4 * blk + 1] = v.w1;
     words[4 * blk + 2] = v.w2; words[4 * blk + 3] = v.w3;
+    if (blk2 < nblk) {
+      words[4 * blk2 + 0] = v2.w0; words[4 * blk2 + 1] = v2.w1;
+      words[4 * blk2 + 2] = v2.w2; words[4 * blk2 + 3] = v2.w3;
+    }
   }
-  __syncthreads();
-  const int64_t e0 = (int64_t)threadIdx.x * K_UNIF;
+  __syncwarp();
   const int a0 = (int)(off & 3);
-  double z[K_UNIF];
+  double sc0[NW], sc1[NW];
   unsigned long long mn = 0x7FF0000000000000ULL;
 #pragma unroll
-  for (int i = 0; i < K_UNIF; ++i) {
-    z[i] = 0.0;
-    if (e0 + i < ne) {
-      z[i] = neglog(u01(words[a0 + e0 + i]));
-      mn = min(mn, (z[i] > 0.0) ? (unsigned long long)__double_as_longlong(z[i]) : 0ull);
-    }
+  for (int w = 0; w < NW; ++w) {
+    const int e0 = 64 * w + 2 * lane;
+    const bool v0 = e0 < ne, v1 = e0 + 1 < ne;
+    const double l0 = neglog(u01(words[a0 + (v0 ? e0 : 0)]));
+    const double l1 = neglog(u01(words[a0 + (v1 ? e0 + 1 : 0)]));
+    const double z0 = v0 ? l0 : 0.0, z1 = v1 ? l1 : 0.0;
+    const unsigned long long m0 = (v0 && !(z0 > 0.0)) ? 0ull
+                                  : (v0 ? (unsigned long long)__double_as_longlong(z0) : 0x7FF0000000000000ULL);
+    const unsigned long long m1 = (v1 && !(z1 > 0.0)) ? 0ull
+                                  : (v1 ? (unsigned long long)__double_as_longlong(z1) : 0x7FF0000000000000ULL);
+    mn = min(mn, min(m0, m1));
+    sc0[w] = z0;
+    sc1[w] = __dadd_rn(z0, z1);
   }
-  block_min_u64(&s_min, mn);
-  double sc[K_UNIF];
-  sc[0] = z[0];
 #pragma unroll
-  for (int i = 1; i < K_UNIF; ++i) sc[i] = __dadd_rn(sc[i - 1], z[i]);
-  // block_fold over the nw warps
-  s_tau[warp * (LANES + 1) + lane] = sc[K_UNIF - 1];
-  __syncthreads();
-  if ((int)threadIdx.x < nw) {
-    double* row = s_tau + threadIdx.x * (LANES + 1);
+  for (int o = 16; o > 0; o >>= 1) mn = min(mn, (unsigned long long)__shfl_xor_sync(FULL, mn, o));
+  __syncwarp();  // the words are consumed: the buffer holds the row totals now
+  double* rows = buf;  // [w][33]: chunk totals of row w, then their bases Q (in place)
+#pragma unroll
+  for (int w = 0; w < NW; ++w) rows[w * (LANES + 1) + lane] = sc1[w];
+  __syncwarp();
+  double* G = buf + WARPS * (LANES + 1);  // row totals
+  if (lane < nw) {
+    double* row = rows + lane * (LANES + 1);
     double acc = 0.0;
 #pragma unroll
-    for (int l = 0; l < LANES; ++l) {
-      const double v = row[l];
-      row[l] = acc;
+    for (int j = 0; j < LANES; ++j) {
+      const double v = row[j];
+      row[j] = acc;
       acc = __dadd_rn(acc, v);
     }
-    s_G[threadIdx.x] = acc;
+    G[lane] = acc;
   }
-  __syncthreads();
-  double R = 0.0, A = 0.0;
-  for (int w = 0; w < nw; ++w) {
-    if (w == warp) R = A;
-    A = __dadd_rn(A, s_G[w]);
-  }
-  const double Q = s_tau[warp * (LANES + 1) + lane];
+  __syncwarp();
+  double A = 0.0, R[NW];
 #pragma unroll
-  for (int i = 0; i < K_UNIF; ++i)
-    if (e0 + i < Nf) su[e0 + i] = __ddiv_rn(__dadd_rn(R, __dadd_rn(Q, sc[i])), A);
-  __syncthreads();
-  uniform_repair(su, Nf, s_min, A, 0, a.status);
-  __syncthreads();
-  for (int64_t i = threadIdx.x; i < Nf; i += blockDim.x) U[f * Nf + i] = su[i];
-  if (threadIdx.x == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every thread has read it
+  for (int w = 0; w < NW; ++w) {
+    R[w] = A;
+    A = __dadd_rn(A, G[w]);
+  }
+  double* Uf = U + f * Nf;
+  const double zmin = __longlong_as_double((long long)mn);
+  const bool rep = !(zmin > __dmul_rn(1e-14, A));  // the exactness check of randkit.py:95
+  const bool vec = (((uintptr_t)Uf) & 15) == 0;
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
+    const double Q = rows[w * (LANES + 1) + lane];
+    const double u0 = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc0[w])), A);
+    const double u1 = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc1[w])), A);
+    const int e0 = 64 * w + 2 * lane;
+    if (vec && e0 + 1 < Nf) {
+      *reinterpret_cast<double2*>(Uf + e0) = make_double2(u0, u1);
+    } else {
+      if (e0 < Nf) Uf[e0] = u0;
+      if (e0 + 1 < Nf) Uf[e0 + 1] = u1;
+    }
+  }
+  if (rep) {  // warp-uniform, rare: lane 0 checks and repairs the stored U serially
+    __syncwarp();
+    double* su = Uf;
+    if (lane == 0 && Nf > 0) {
+      bool b2 = (su[0] <= 0.0) || (su[Nf - 1] >= 1.0);
+      for (int64_t i = 1; !b2 && i < Nf; ++i) b2 = !(__dsub_rn(su[i], su[i - 1]) > 0.0);
+      if (b2) {
+        double lo = 0.0;
+        for (int64_t i = 0; i < Nf; ++i) {
+          if (su[i] <= lo) su[i] = nextafter(lo, 1.0);
+          lo = su[i];
+        }
+        double hi = 1.0;
+        for (int64_t i = Nf - 1; i >= 0; --i) {
+          if (su[i] >= hi) su[i] = nextafter(hi, 0.0);
+          hi = su[i];
+        }
+        atomicOr(a.status, DRS_ST_REPAIRED);
+      }
+    }
+  }
+  if (lane == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every lane has read it
 }
 
 __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
@@ -505,8 +555,17 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
       c_usmem = usmem;
     }
     if (ntu == 1) {
-      const int nw = (int)cdiv(cdiv(Nf + 1, K_UNIF), LANES);
-      k_batched_uniforms1<<<(unsigned)B, (unsigned)(nw * LANES), 0, st>>>(a, Ub);
+      const unsigned g = (unsigned)cdiv(B, UW_FILTERS), t = UW_FILTERS * LANES;
+      switch ((int)cdiv(Nf + 1, 2 * LANES)) {
+        case 1: k_batched_uniforms_warp<1><<<g, t, 0, st>>>(a, Ub); break;
+        case 2: k_batched_uniforms_warp<2><<<g, t, 0, st>>>(a, Ub); break;
+        case 3: k_batched_uniforms_warp<3><<<g, t, 0, st>>>(a, Ub); break;
+        case 4: k_batched_uniforms_warp<4><<<g, t, 0, st>>>(a, Ub); break;
+        case 5: k_batched_uniforms_warp<5><<<g, t, 0, st>>>(a, Ub); break;
+        case 6: k_batched_uniforms_warp<6><<<g, t, 0, st>>>(a, Ub); break;
+        case 7: k_batched_uniforms_warp<7><<<g, t, 0, st>>>(a, Ub); break;
+        default: k_batched_uniforms_warp<8><<<g, t, 0, st>>>(a, Ub); break;
+      }
     } else {
       k_batched_uniforms<<<(unsigned)B, THREADS, usmem, st>>>(a, Ub);
     }
