@@ -15,6 +15,8 @@
 // The table pass reads w twice and writes W once (24 bytes per entry); the
 // uniform pass generates each draw once, writes the in-tile sums in pass 1 and
 // turns them into U in pass 2 (24 bytes per u).
+#include <algorithm>
+
 #include "drs_common.cuh"
 
 namespace drs {
@@ -70,16 +72,17 @@ constexpr int CHAIN_MAX_GROUPS = 8192;    // nt <= 2^18 tiles
 constexpr size_t CHAIN_SMEM = (size_t)CHAIN_CHUNK * 8 + (size_t)CHAIN_MAX_GROUPS * 8;
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64_t nt, int mode,
-                                                               int32_t* status_out, double* total_out) {
+                                                               int32_t* status_out, double* total_out,
+                                                               int64_t chunk) {
   extern __shared__ __align__(16) double csm[];
-  double* sa = csm;                // [CHAIN_CHUNK] tile totals -> exclusive in-group folds
-  double* sE = csm + CHAIN_CHUNK;  // [ng] group totals -> group bases
+  double* sa = csm;          // [chunk] tile totals -> exclusive in-group folds
+  double* sE = csm + chunk;  // [ng] group totals -> group bases
   __shared__ unsigned long long s_min;
   if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
   const int64_t ng = cdiv(nt, GROUP_TILES);
   unsigned long long mn = 0x7FF0000000000000ULL;
-  for (int64_t c0 = 0; c0 < nt; c0 += CHAIN_CHUNK) {
-    const int64_t c1 = (c0 + CHAIN_CHUNK < nt) ? c0 + CHAIN_CHUNK : nt;
+  for (int64_t c0 = 0; c0 < nt; c0 += chunk) {
+    const int64_t c1 = (c0 + chunk < nt) ? c0 + chunk : nt;
     // 1. stage the chunk's tile totals (coalesced, all loads in flight)
     for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) {
       sa[t - c0] = ws.agg[t];
@@ -150,7 +153,11 @@ void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double
     cudaFuncSetAttribute(k_chain_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
     attr = true;
   }
-  k_chain_groups<<<1, CHAIN_THREADS, CHAIN_SMEM, st>>>(s, nt, mode, status, total);
+  // shared memory sized to the call (whole groups of tiles, then the group
+  // totals): small chains launch without reconfiguring a 192 KB carve-out
+  const int64_t chunk = std::min<int64_t>(CHAIN_CHUNK, cdiv(nt, GROUP_TILES) * GROUP_TILES);
+  const size_t smem = (size_t)(chunk + cdiv(nt, GROUP_TILES)) * 8;
+  k_chain_groups<<<1, CHAIN_THREADS, smem, st>>>(s, nt, mode, status, total, chunk);
 }
 
 // exclusive chained prefix of tile t applied to an in-tile value y
@@ -456,8 +463,8 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, S
 // after pass 2: the repair when pass 2 found collapse sites, the status word,
 // the device stream advance, counters back to zero
 __global__ void k_unif_finalize(ScanWS ws, int64_t n, double* U, int32_t* status_out, uint64_t* offset_dev) {
-  const uint32_t nsites = ws.hdr->nsites;
-  const uint32_t top = ws.hdr->top;
+  const uint32_t nsites = *(volatile uint32_t*)&ws.hdr->nsites;
+  const uint32_t top = *(volatile uint32_t*)&ws.hdr->top;
   int32_t st = 0;
   if (ws.hdr->need && (nsites > 0 || top)) {
     repair_sites(U, n, ws, nsites, true);  // the backward pass stops at the first untouched entry
