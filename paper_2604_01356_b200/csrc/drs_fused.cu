@@ -499,12 +499,14 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   extern __shared__ __align__(128) double sidx[];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t sbytes = (uint32_t)(sl.count * 8);
+  pdl_wait();
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, sbytes);
     if (sbytes) bulk_g2s(sidx, idx + sl.base, sbytes, &bar);
   }
   __syncthreads();
+  pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
   for (int64_t base = lo + (int64_t)blockIdx.x * 2 * blockDim.x; base < hi; base += (int64_t)gridDim.x * 2 * blockDim.x) {
@@ -544,7 +546,7 @@ int launch_index_sm(const double* W, const double* idx, int64_t M, const double*
   }
   const int64_t chunks = cdiv(N, 512);
   const int64_t grid = chunks < (int64_t)sms * c_per ? chunks : (int64_t)sms * c_per;
-  k_match_index_sm<<<(unsigned)grid, 256, smem, st>>>(W, idx, d, sl, u, N, out, rng, shift);
+  launch_pdl(k_match_index_sm, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 

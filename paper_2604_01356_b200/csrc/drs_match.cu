@@ -136,6 +136,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   const bool last = (j0 + len == M);
   const int len_even = len & ~1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_wait();
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
     if (lane == 0) s_ie = v;
   }
   __syncthreads();
+  pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t ib = s_ib, ie = s_ie;
   if (ie - ib <= 2 * MT_THREADS) {
@@ -280,7 +282,7 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
   int tw = MT_TW;
   while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
   const size_t smem = (size_t)(tw + 2 * MT_UC) * sizeof(double);
-  k_merge_tiles<<<(unsigned)cdiv(M, tw), MT_THREADS, smem, st>>>(W, M, U, N, out, tw);
+  launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, U, N, out, tw);
   return launch_rc();
 }
 

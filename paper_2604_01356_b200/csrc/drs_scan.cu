@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
                                                                int32_t* status_out, double* total_out,
                                                                int64_t chunk) {
   extern __shared__ __align__(16) double csm[];
+  pdl_wait();
+  pdl_trigger();  // one CTA: the next grid may take the other SMs now
   double* sa = csm;          // [chunk] tile totals -> exclusive in-group folds
   double* sE = csm + chunk;  // [ng] group totals -> group bases
   __shared__ unsigned long long s_min;
@@ -157,7 +159,7 @@ void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double
   // totals): small chains launch without reconfiguring a 192 KB carve-out
   const int64_t chunk = std::min<int64_t>(CHAIN_CHUNK, cdiv(nt, GROUP_TILES) * GROUP_TILES);
   const size_t smem = (size_t)(chunk + cdiv(nt, GROUP_TILES)) * 8;
-  k_chain_groups<<<1, CHAIN_THREADS, smem, st>>>(s, nt, mode, status, total, chunk);
+  launch_pdl(k_chain_groups, dim3(1), dim3(CHAIN_THREADS), smem, st, s, nt, mode, status, total, chunk);
 }
 
 // exclusive chained prefix of tile t applied to an in-tile value y
@@ -374,6 +376,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   __shared__ FoldSmem fs;
   __shared__ unsigned long long s_min;
   __shared__ uint64_t s_words[Src::SMEM_WORDS];
+  pdl_wait();
   if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
   const int64_t t = blockIdx.x;
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
@@ -395,6 +398,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
     ws.agg[t] = A;
     ws.incl[t] = __longlong_as_double((long long)s_min);  // folded by k_chain_groups
   }
+  pdl_trigger();
   double v[K_UNIF];
 #pragma unroll
   for (int i = 0; i < K_UNIF; ++i) v[i] = __dadd_rn(R, __dadd_rn(Q, sc[i]));
@@ -412,6 +416,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
 // the device stream advance follow in k_unif_finalize).
 __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, ScanWS ws, double* __restrict__ U) {
   __shared__ double s_last[WARPS];
+  pdl_wait();
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
   const int64_t t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -433,6 +438,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, S
       if (e0 + i < n) U[e0 + i] = u[i];
     }
   }
+  pdl_trigger();
   if (need) {
     // previous U for each element: inside the chunk, from lane-1, from the
     // previous warp, or from the previous tile's last Z
@@ -463,6 +469,8 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, S
 // after pass 2: the repair when pass 2 found collapse sites, the status word,
 // the device stream advance, counters back to zero
 __global__ void k_unif_finalize(ScanWS ws, int64_t n, double* U, int32_t* status_out, uint64_t* offset_dev) {
+  pdl_wait();
+  pdl_trigger();
   const uint32_t nsites = *(volatile uint32_t*)&ws.hdr->nsites;
   const uint32_t top = *(volatile uint32_t*)&ws.hdr->top;
   int32_t st = 0;
@@ -555,10 +563,10 @@ static int sorted_impl(const Src& src, int64_t n, double* U, int32_t* status, vo
   if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
   if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
   const ScanWS s = carve(ws, ws_bytes);
-  k_unif_pass1<Src><<<(unsigned)nt, THREADS, 0, st>>>(src, n, s, U);
+  launch_pdl(k_unif_pass1<Src>, dim3((unsigned)nt), dim3(THREADS), 0, st, src, n, s, U);
   launch_chain(s, nt, 1, nullptr, nullptr, st);
-  k_unif_pass2<<<(unsigned)nt, THREADS, 0, st>>>(n, nt, s, U);
-  k_unif_finalize<<<1, 1, 0, st>>>(s, n, U, status, offset_dev);
+  launch_pdl(k_unif_pass2, dim3((unsigned)nt), dim3(THREADS), 0, st, n, nt, s, U);
+  launch_pdl(k_unif_finalize, dim3(1), dim3(1), 0, st, s, n, U, status, offset_dev);
   return launch_rc();
 }
 

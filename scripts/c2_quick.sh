@@ -2,7 +2,7 @@
 mkdir -p gpurun_out/c2
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1; echo build rc=$?
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/c2/pytest.log 2>&1; echo pytest rc=$?; tail -3 gpurun_out/c2/pytest.log
-for spec in "c2 dac auto" "c2 ccf auto" "c5 dac auto"; do
+for spec in "c2 dac auto" "c2 ccf auto" "c5 dac auto" "c3 ccf auto"; do
   set -- $spec
   timeout 300 python bench.py --config $1 --sampler $2 --mode $3 --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/c2/bench_$1_$2_$3.json 2> gpurun_out/c2/bench_$1_$2_$3.err; echo bench $spec rc=$?
   python scripts/summarize.py gpurun_out/c2/bench_$1_$2_$3.json
