@@ -290,6 +290,8 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
 // bucket, a bisection among level kt's entries (L2-resident, <= 16384 of them);
 // the storage tail past bucket B + 1 is zeroed
 __global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ idx, IndexDesc d) {
+  pdl_wait();
+  pdl_trigger();
   int32_t* G = reinterpret_cast<int32_t*>(idx + d.toff);
   const int64_t cap = 2 * tg_doubles(d), nb = ((int64_t)1 << d.tshift) + 2;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ id
 int launch_top_guide(int64_t M, double* idx, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
   if (!d.kt) return DRS_OK;
-  k_build_top_guide<<<(unsigned)cdiv(2 * tg_doubles(d), 256), 256, 0, st>>>(idx, d);
+  launch_pdl(k_build_top_guide, dim3((unsigned)cdiv(2 * tg_doubles(d), 256)), dim3(256), 0, st, idx, d);
   return launch_rc();
 }
 

@@ -202,6 +202,7 @@ __global__ void __launch_bounds__(256) k_max_logw(const double* __restrict__ lw,
   __shared__ unsigned long long s_key;
   __shared__ int s_nan;
   __shared__ bool s_last;
+  pdl_wait();
   if (threadIdx.x == 0) { s_key = 0; s_nan = 0; }
   __syncthreads();
   unsigned long long key = 0;
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
   __shared__ __align__(8) uint64_t bar;
   __shared__ FoldSmem fs;
   const int64_t t = blockIdx.x;
+  pdl_wait();
   const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
   if (LOGW) {
     exp_shift_tile(sm, len, ws.hdr->wmax);  // each thread transforms its own chunk
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(THREADS) k_table_pass1(const double* __restric
     for (int i = 0; i < K_TABLE; ++i) bad |= !(chunk[i] >= 0.0);
   double Q, R;
   const double A = block_fold(s, fs, Q, R);
+  pdl_trigger();
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.hdr->status, (uint32_t)DRS_ST_INVALID_WEIGHT);
   if (threadIdx.x == 0) ws.agg[t] = A;
   if (LOGW && threadIdx.x == 0) bulk_commit_wait();  // smem stays valid until the store has read it
@@ -312,6 +315,10 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
   for (int i = 1; i < K_TABLE; ++i) s = __dadd_rn(s, chunk[i]);
   double Q, R;
   block_fold(s, fs, Q, R);
+  // everything above reads only the weights (produced before the previous
+  // launch): under programmatic launch it overlaps the chain kernel
+  pdl_wait();
+  pdl_trigger();
   const double C = ws.grp[t / GROUP_TILES], D = ws.incl[t];
   const double T = ws.hdr->total;
   const int64_t jb = t * TS + (int64_t)(warp * LANES + lane) * K_TABLE;
@@ -652,9 +659,10 @@ int dr_build_table(const double* w, int64_t M, double* W, double* idx, int32_t* 
   const ScanWS s = carve(ws, ws_bytes);
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
-  k_table_pass1<false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, s, nullptr);
+  launch_pdl(k_table_pass1<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, (double*)nullptr);
   launch_chain(s, nt, 0, status, nullptr, st);
-  k_table_pass2<false, false><<<(unsigned)nt, THREADS, smem, st>>>(w, M, nt, s, W, idx, d, status, nullptr);
+  launch_pdl(k_table_pass2<false, false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, nt, s, W, idx, d,
+             status, (double*)nullptr);
   if (launch_rc()) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
 }
@@ -674,10 +682,11 @@ int dr_build_table_log(const double* logw, int64_t M, double* W, double* idx, in
   const int smem = THREADS * K_TABLE * 8;
   const int64_t mb = cdiv(M, 256 * 8);
   const unsigned mgrid = (unsigned)(mb < nt ? (mb < 1 ? 1 : mb) : nt);  // partials fit in agg[nt]
-  k_max_logw<<<mgrid < 1184 ? mgrid : 1184, 256, 0, st>>>(logw, M, s);
-  k_table_pass1<true><<<(unsigned)nt, THREADS, smem, st>>>(logw, M, s, W);  // w -> W
+  launch_pdl(k_max_logw, dim3(mgrid < 1184 ? mgrid : 1184), dim3(256), 0, st, logw, M, s);
+  launch_pdl(k_table_pass1<true>, dim3((unsigned)nt), dim3(THREADS), smem, st, logw, M, s, W);  // w -> W
   launch_chain(s, nt, 0, status, nullptr, st);
-  k_table_pass2<false, false><<<(unsigned)nt, THREADS, smem, st>>>(W, M, nt, s, W, idx, d, status, nullptr);
+  launch_pdl(k_table_pass2<false, false>, dim3((unsigned)nt), dim3(THREADS), smem, st, (const double*)W, M, nt, s,
+             W, idx, d, status, (double*)nullptr);
   if (launch_rc()) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
 }
@@ -694,9 +703,10 @@ int dr_shard_scan(const double* w_shard, int64_t Mg, double* S, double* Tg, int3
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
   const IndexDesc d = make_index_desc(Mg);
-  k_table_pass1<false><<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, s, nullptr);
+  launch_pdl(k_table_pass1<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w_shard, Mg, s, (double*)nullptr);
   launch_chain(s, nt, 0, status, Tg, st);
-  k_table_pass2<true, false><<<(unsigned)nt, THREADS, smem, st>>>(w_shard, Mg, nt, s, S, nullptr, d, status, Tg);
+  launch_pdl(k_table_pass2<true, false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w_shard, Mg, nt, s, S,
+             (double*)nullptr, d, status, Tg);
   return launch_rc();
 }
 
