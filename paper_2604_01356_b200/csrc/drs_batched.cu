@@ -4,10 +4,11 @@
 // build_weight_table (cdf.py:59-89) + dac_sampler (samplers.py:262-266) per
 // filter.  Here two launches serve the whole bank:
 //
-//   k_batched_uniforms  one small CTA per filter draws the N_f + 1 Philox
-//     spacings (each Philox block once), folds them with the association of
-//     dr_sorted_uniforms, normalises, repairs collapses and writes U[f]; small
-//     CTAs (8+ per SM) keep this compute-bound step wide;
+//   k_batched_uniforms_warp (N_f + 1 <= 512; k_batched_uniforms beyond) one
+//     warp per filter draws the N_f + 1 Philox spacings (each Philox block
+//     once), folds them with the association of dr_sorted_uniforms,
+//     normalises, repairs collapses and writes U[f]; 24+ warps per SM keep
+//     this compute-bound step wide;
 //   k_resample_batched  one thread-block CLUSTER per filter, one CTA per table
 //     tile of the chained scan (THREADS x K_TABLE = 8448 weights; M_f = 16384
 //     is a 2-CTA cluster):
@@ -20,11 +21,14 @@
 //     totals (Q, R) -- the chained association of dr_build_table, so W is
 //     bit-identical to the single-filter path;
 //   * the tile totals A_r are exchanged through distributed shared memory
-//     (st.shared::cluster + one cluster barrier); every CTA then folds the
+//     (st.async into every peer, completing the peer's transaction barrier;
+//     no cluster-wide barrier after the start); every CTA then folds the
 //     tile prefixes P_r and the filter total T in tile order;
 //   * CTA r answers exactly the draws u with W_end(r-1) < u <= W_end(r),
-//     W_end(r) = min(P_{r+1} / T, 1) being W at the tile's last entry, by a
-//     bisection over its lane-chunk ends and then inside the chunk, whose
+//     W_end(r) = min(P_{r+1} / T, 1) being W at the tile's last entry, i.e.
+//     P_r < s*(u) <= P_{r+1}: every thread forms s*(u) for its draws and keeps
+//     those of its tile, then a bisection over its lane-chunk ends and inside
+//     the chunk, whose
 //     probes form W_j = min((P_r + (R + (Q + s2_j))) / T, 1) on the fly
 //     (a few divisions per draw instead of one per weight; all of W only on
 //     request).
@@ -47,15 +51,47 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
-  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 // store v into the shared-memory word `local` of CTA `rank` of this cluster
-__device__ __forceinline__ void st_cluster_f64(double* local, uint32_t rank, double v) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
-  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(remote), "d"(v) : "memory");
+// and complete 8 bytes of that CTA's transaction barrier `bar` (st.async: no
+// cluster barrier, no fence; the receiver waits on its own barrier)
+__device__ __forceinline__ void st_async_cluster_f64(double* local, uint64_t* bar, uint32_t rank, double v) {
+  uint32_t rdst, rbar;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rdst) : "r"(smem_u32(local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(rdst),
+               "l"((unsigned long long)__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+// wait for phase `phase` of a barrier completed by peers of the cluster
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  }
+}
+
+// s*(x): the least double s with fl(s / T) >= x (division is monotone in s),
+// so that fl(S / T) < x <=> S < s*(x).  The candidates fl(x T) and its two
+// neighbours are divided together; a longer walk by ulps is rare.  T must be
+// positive and finite.
+__device__ __forceinline__ double s_star(double x, double T) {
+  const double sx = __dmul_rn(x, T);
+  const double sm = nextafter(sx, -dinf()), sp = nextafter(sx, dinf());
+  const double q0 = __ddiv_rn(sx, T), qm = __ddiv_rn(sm, T), qp = __ddiv_rn(sp, T);
+  if (q0 >= x) {
+    if (!(qm >= x)) return sx;
+    double r = sm;
+    for (double q = nextafter(sm, -dinf()); __ddiv_rn(q, T) >= x; q = nextafter(q, -dinf())) r = q;
+    return r;
+  }
+  if (qp >= x) return sp;
+  double r = sp;
+  do r = nextafter(r, dinf()); while (__ddiv_rn(r, T) < x);
+  return r;
 }
 
 // the exactness check and repair of randkit.py:95-116 on a filter's U (in
@@ -325,12 +361,11 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 6) k_batched_uniforms_warp
 
 __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t bar, baru;
+  __shared__ __align__(8) uint64_t bar, baru, barx;
   __shared__ FoldSmem fs;         // fold of the table tile
   __shared__ double s_R[WARPS];   // warp bases R of the table tile
   __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
   __shared__ int s_bad;
-  __shared__ int s_range[2];
   __shared__ double s_cend[THREADS];  // S at each lane chunk's last entry
   const int64_t Mf = a.Mf, Nf = a.Nf, ne = Nf + 1;
   const int r = (int)cluster_rank();
@@ -348,6 +383,8 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   const bool tmau = Nf > 0 && ((((uintptr_t)ut) | ((uintptr_t)Nf * 8)) & 15) == 0;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&barx, 1);  // the peers' tile totals (st.async, 8 bytes each)
+    mbar_init(&baru, 1);  // U[f]
     if (tma) {
       mbar_expect_tx(&bar, (uint32_t)len * 8u);
       bulk_g2s(sw, wt, (uint32_t)len * 8u, &bar);
@@ -363,26 +400,9 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   // shared memory only once every CTA of the cluster is running
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 
-  // ---- 1. this filter's sorted uniforms.  The launch may overlap the tail of
-  // k_batched_uniforms (programmatic dependent launch): the weight copy above
-  // is already in flight; U is read only after the uniforms grid completed.
-  if (Nf > 0) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (tmau) {
-      if (threadIdx.x == 0) {
-        mbar_init(&baru, 1);
-        mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
-        bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
-      }
-      __syncthreads();
-      mbar_wait(&baru, 0);
-    } else {
-      for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = a.Uin[f * Nf + i];
-      __syncthreads();
-    }
-  }
-
-  // ---- 2. the table sweep over this CTA's tile
+  // ---- 1. the table sweep over this CTA's tile.  The launch may overlap the
+  // uniforms kernel (programmatic dependent launch): the weights were written
+  // before it, so the sweep and the in-tile fold run before waiting on U.
   STAMP(1);
   if (tma) mbar_wait(&bar, 0);
   STAMP(2);
@@ -416,12 +436,34 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   if (lane == 0) s_R[warp] = R;
   if (bad) s_bad = 1;
 
+  // ---- 2. this filter's sorted uniforms (after the uniforms grid completed);
+  // the copy overlaps the exchange below
+  if (Nf > 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tmau) {
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
+        bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
+      }
+    } else {
+      for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = a.Uin[f * Nf + i];
+    }
+  }
+
   STAMP(3);
-  // ---- 3. exchange the tile totals through distributed shared memory
+  // ---- 3. exchange the tile totals through distributed shared memory: each
+  // CTA stores its total into every peer with st.async, completing 8 bytes of
+  // the peer's transaction barrier, and waits on its own
   asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-  if (threadIdx.x == 0)
-    for (int q = 0; q < a.ntt; ++q) st_cluster_f64(&s_A[r], (uint32_t)q, A);
-  cluster_sync_all();  // also the CTA barrier for sQ / s_R / s_bad / su
+  if (threadIdx.x == 0) {
+    s_A[r] = A;
+    mbar_expect_tx(&barx, 8u * (uint32_t)(a.ntt - 1));
+    for (int q = 0; q < a.ntt; ++q)
+      if (q != r) st_async_cluster_f64(&s_A[r], &barx, (uint32_t)q, A);
+  }
+  mbar_wait_cluster(&barx, 0);
+  if (Nf > 0 && tmau) mbar_wait(&baru, 0);
+  __syncthreads();  // sQ / s_R / s_bad / su / s_A
   double Pr = 0.0, T = 0.0;
   for (int q = 0; q < a.ntt; ++q) {
     if (q == r) Pr = T;
@@ -449,42 +491,16 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   // the least double s with fl(s / T) >= u (division is monotone in s), so the
   // probes need no division and no clamp (the pinned last weight, W = 1 >= u,
   // is never a probe of a lower-bound bisection: m < hi always).
-  if (Nf > 0) {
-    // u in (W_end(r-1), W_end(r)]; W_end(r-1) = min(P_r / T, 1); the last tile takes the rest
-    if (warp < 2) {
-      const bool first = (warp == 0);
-      int v;
-      if (first ? (r == 0) : (r == a.ntt - 1)) {
-        v = first ? 0 : (int)Nf;
-      } else {
-        const double key = fmin(__ddiv_rn(first ? Pr : Pnext, T), 1.0);
-        int lo = 0, hi = (int)Nf;  // #(su[i] <= key): 32-ary narrowing
-        while (hi - lo > 32) {
-          const int step = (hi - lo + 31) / 32;
-          const int p = lo + (lane + 1) * step - 1;
-          const int cnt = __popc(__ballot_sync(FULL, p < hi && su[p] <= key));
-          const int nhi = lo + (cnt + 1) * step - 1;
-          lo += cnt * step;
-          hi = nhi < hi ? nhi : hi;
-        }
-        v = lo + __popc(__ballot_sync(FULL, lo + lane < hi && su[lo + lane] <= key));
-      }
-      if (lane == 0) s_range[warp] = v;
-    }
-    __syncthreads();
-    const int ib = s_range[0], ie = s_range[1];
-    for (int i = ib + threadIdx.x; i < ie; i += THREADS) {
-      const double x = su[i];
-      // s*(x): start at fl(x T), step by ulps (one or two divisions in practice)
-      double sx = __dmul_rn(x, T);
-      if (__ddiv_rn(sx, T) >= x) {
-        for (double p = nextafter(sx, -dinf()); __ddiv_rn(p, T) >= x; p = nextafter(p, -dinf())) sx = p;
-      } else {
-        do sx = nextafter(sx, dinf()); while (__ddiv_rn(sx, T) < x);
-      }
+  if (Nf > 0 && T > 0.0 && T < dinf()) {
+    // every thread takes draws i = tid, tid + 256, ... of the filter: u lands in
+    // this tile iff P_r < s*(u) <= P_{r+1} (u in (W_end(r-1), W_end(r)]); the
+    // first tile takes everything below, the last everything above
+    const int nch = (len + K_TABLE - 1) / K_TABLE;
+    for (int i = threadIdx.x; i < (int)Nf; i += THREADS) {
+      const double sx = s_star(su[i], T);
+      if (!((r == 0 || Pr < sx) && (r == a.ntt - 1 || sx <= Pnext))) continue;
       // the chunk: first chunk whose last S is >= s*(x) (the tile's last
       // chunk otherwise), then the entry inside it
-      const int nch = (len + K_TABLE - 1) / K_TABLE;
       int clo = 0, chi = nch - 1;
       while (clo < chi) {
         const int m = (clo + chi) >> 1;
