@@ -45,7 +45,7 @@ t = buf.reshape(nc, 16)[:, :6].astype(np.float64)
 t0 = t[:, 0].min()
 t = (t - t0) / 1e3
 span = t[:, 5].max()
-names = ["start", "U loaded", "tile landed", "sweep+fold", "cluster exchange", "search+write"]
+names = ["start", "(init)", "tile landed", "sweep+fold (+U copy issued)", "exchange (+U landed)", "s* + search + write"]
 print(f"c4: {nc} CTAs, kernel span {span:.1f} us")
 for k in range(1, 6):
     d = t[:, k] - t[:, k - 1]
