@@ -116,14 +116,6 @@ __device__ __forceinline__ void uniform_repair(double* su, int64_t Nf, unsigned 
   if (r == 0) atomicOr(status, DRS_ST_REPAIRED);
 }
 
-// valid weight <=> 0 <= x < inf (-0.0 included, NaN excluded); screened from
-// the high word: any sign bit (exact re-check follows) or an all-ones exponent
-__device__ __forceinline__ void track_hi(double x, uint32_t& any_sign, uint32_t& max_mag) {
-  const uint32_t hi = (uint32_t)__double2hiint(x);
-  any_sign |= hi;
-  max_mag = max(max_mag, hi & 0x7FFFFFFFu);
-}
-
 struct BatchedArgs {
   const double* w;
   int64_t B, Mf, Nf;
@@ -406,7 +398,11 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   STAMP(1);
   if (tma) mbar_wait(&bar, 0);
   STAMP(2);
-  uint32_t any_sign = 0, max_mag = 0;
+  // valid weight <=> 0 <= x < inf (-0.0 included, NaN excluded): one OR of
+  // the high words per weight catches any sign bit, and an infinite or NaN
+  // weight makes the chunk sum non-finite; either sends the chunk to an exact
+  // re-check of the raw weights (a finite overflow of the sum is not invalid)
+  uint32_t any_sign = 0;
   const int c0 = threadIdx.x * K_TABLE;
   double* chunk = sw + c0;
   double s = 0.0;
@@ -414,7 +410,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
 #pragma unroll
     for (int i = 0; i < K_TABLE; ++i) {
       const double x = chunk[i];
-      track_hi(x, any_sign, max_mag);
+      any_sign |= (uint32_t)__double2hiint(x);
       s = (i == 0) ? x : __dadd_rn(s, x);
       chunk[i] = s;
     }
@@ -422,14 +418,17 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
 #pragma unroll
     for (int i = 0; i < K_TABLE; ++i) {
       const double x = chunk[i];
-      track_hi(x, any_sign, max_mag);
+      any_sign |= (uint32_t)__double2hiint(x);
       s = (i == 0) ? x : __dadd_rn(s, x);
       if (c0 + i < len) chunk[i] = s;
     }
   }
-  bool bad = max_mag >= 0x7FF00000u;  // inf or NaN
-  if (any_sign & 0x80000000u)         // a sign bit: re-check the raw weights (-0.0 is valid)
-    for (int i = 0; i < K_TABLE && c0 + i < len; ++i) bad |= !(wt[c0 + i] >= 0.0);
+  bool bad = false;
+  if ((any_sign & 0x80000000u) || !(s < dinf()))
+    for (int i = 0; i < K_TABLE && c0 + i < len; ++i) {
+      const double x = wt[c0 + i];
+      bad |= !(x >= 0.0) || x == dinf();
+    }
   double Q, R;
   const double A = block_fold(s, fs, Q, R);
   sQ[threadIdx.x] = Q;
