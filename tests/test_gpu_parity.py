@@ -367,6 +367,12 @@ def test_batched_invalid_weights_raise(drs):
     w[3, 5] = -1.0
     with pytest.raises(ValueError, match="invalid weight"):
         drs.resample_batched(w, 8, [drs.RngStream(1, (b,)) for b in range(10)])
+    # a negative filter total (and NaN / inf totals): the search is skipped, no hang
+    for bad in (-1.0, np.nan, np.inf):
+        w = np.ones((300, 16384))
+        w[7] = bad
+        with pytest.raises(ValueError, match="invalid weight"):
+            drs.resample_batched(w, 256, [drs.RngStream(2, (b,)) for b in range(300)])
     w = np.ones((10, 100))
     w[7] = 0.0
     with pytest.raises(ValueError, match="degenerate distribution"):
