@@ -552,11 +552,8 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
   cudaStream_t st = (cudaStream_t)stream;
   if (cudaMemsetAsync(status, 0, sizeof(int32_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
   if (B == 0) return DRS_OK;
-  static size_t c_smem = 0;  // attribute raised once per size (only launches under graph capture)
-  if (c_smem < smem) {
-    cudaFuncSetAttribute(k_resample_batched, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    c_smem = smem;
-  }
+  static SmemLimit lim;  // raised once per size and device (only launches under graph capture)
+  lim.raise((const void*)k_resample_batched, smem);
   // U: the caller's buffer, else stream-ordered scratch (graph-capturable)
   double* Ub = U;
   if (!Ub && Nf > 0 && cudaMallocAsync((void**)&Ub, sizeof(double) * (size_t)(B * Nf), st) != cudaSuccess)
@@ -564,11 +561,8 @@ extern "C" int dr_resample_batched(const double* w, int64_t B, int64_t Mf, int64
   BatchedArgs a{w, B, Mf, Nf, keys, advance, W, Ub, Ub, out, status, ntt, ntu};
   if (Nf > 0) {
     const size_t usmem = (size_t)((Nf + 1 + 8 + 15) & ~(int64_t)15) * 8;
-    static size_t c_usmem = 0;
-    if (c_usmem < usmem) {
-      cudaFuncSetAttribute(k_batched_uniforms, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)usmem);
-      c_usmem = usmem;
-    }
+    static SmemLimit ulim;
+    ulim.raise((const void*)k_batched_uniforms, usmem);
     if (ntu == 1) {
       const unsigned g = (unsigned)cdiv(B, UW_FILTERS), t = UW_FILTERS * LANES;
       switch ((int)cdiv(Nf + 1, 2 * LANES)) {

@@ -529,41 +529,25 @@ int launch_index_sm(const double* W, const double* idx, int64_t M, const double*
                     cudaStream_t st, const int64_t* rng, int64_t shift) {
   const IndexDesc d = make_index_desc(M);
   const SmemLevels sl = plan_smem_levels(d, DRS_MATCH_SMEM_CAP);
-  static int sms = 0;
-  static size_t c_smem = (size_t)-1;
-  static int c_per = 0;
+  static SmemLimit lim;
+  static OccupancyCache occ;
   const size_t smem = (size_t)sl.count * 8;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_match_index_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
-  }
-  if (c_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, k_match_index_sm, 256, smem);
-    c_smem = smem;
-    if (c_per < 1) c_per = 1;
-  }
+  lim.raise((const void*)k_match_index_sm, SIDX_CAP * 8);
+  const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_match_index_sm, 256, smem);
   const int64_t chunks = cdiv(N, 512);
-  const int64_t grid = chunks < (int64_t)sms * c_per ? chunks : (int64_t)sms * c_per;
+  const int64_t grid = chunks < cap ? chunks : cap;
   launch_pdl(k_match_index_sm, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 
 __global__ void k_advance_offset(uint64_t* p, uint64_t by) { *p += by; }
 
-static int g_coop_blocks = -1;
-
+// co-resident CTAs of the cooperative fused kernel on this device
 static int coop_capacity() {
-  if (g_coop_blocks < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_dac_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_dac_fused, THREADS, SIDX_CAP * 8);
-    g_coop_blocks = sms * per;
-  }
-  return g_coop_blocks;
+  static SmemLimit lim;
+  static OccupancyCache occ;
+  lim.raise((const void*)k_dac_fused, SIDX_CAP * 8);
+  return drs_sm_count() * occ.get((const void*)k_dac_fused, THREADS, SIDX_CAP * 8);
 }
 
 }  // namespace drs
@@ -646,23 +630,13 @@ int dr_sample_binary_dev(const double* W, const double* idx, int64_t M, uint64_t
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
   const SmemLevels sl = plan_smem_levels(d);
   // persistent grid: as many CTAs as fit with this shared-memory size
-  static int sms = 0;
-  static size_t c_smem = (size_t)-1;
-  static int c_per = 0;
+  static SmemLimit lim;
+  static OccupancyCache occ;
   const size_t smem = (size_t)sl.count * 8;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_sample_binary_sm, cudaFuncAttributeMaxDynamicSharedMemorySize, SIDX_CAP * 8);
-  }
-  if (c_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c_per, k_sample_binary_sm, 256, smem);
-    c_smem = smem;
-    if (c_per < 1) c_per = 1;
-  }
+  lim.raise((const void*)k_sample_binary_sm, SIDX_CAP * 8);
+  const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_sample_binary_sm, 256, smem);
   const int64_t chunks = cdiv(N, 512);
-  const int64_t grid = chunks < (int64_t)sms * c_per ? chunks : (int64_t)sms * c_per;
+  const int64_t grid = chunks < cap ? chunks : cap;
   k_sample_binary_sm<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(W, idx, d, sl, k0, k1, offset,
                                                                           offset_dev, N, out);
   if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;

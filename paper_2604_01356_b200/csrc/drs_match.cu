@@ -269,14 +269,9 @@ __global__ void k_lower_bound_range(const double* __restrict__ W, int64_t lo, in
 
 int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
                  cudaStream_t st) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_merge_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)((MT_TW + 2 * MT_UC) * sizeof(double)));
-  }
+  static SmemLimit lim;
+  lim.raise((const void*)k_merge_tiles, (MT_TW + 2 * MT_UC) * sizeof(double));
+  const int sms = drs_sm_count();
   // tiles of up to 4096 entries; smaller for small tables so that every SM
   // gets >= ~6 tiles to overlap
   int tw = MT_TW;

@@ -150,11 +150,8 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
 
 void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total,
                   cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chain_groups, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHAIN_SMEM);
-    attr = true;
-  }
+  static SmemLimit lim;
+  lim.raise((const void*)k_chain_groups, CHAIN_SMEM);
   // shared memory sized to the call (whole groups of tiles, then the group
   // totals): small chains launch without reconfiguring a 192 KB carve-out
   const int64_t chunk = std::min<int64_t>(CHAIN_CHUNK, cdiv(nt, GROUP_TILES) * GROUP_TILES);
@@ -543,15 +540,13 @@ static int launch_rc() {
   return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 
-static bool g_attr_done = false;
 static void set_attrs() {
-  if (g_attr_done) return;
-  const int smem = THREADS * K_TABLE * 8;
-  cudaFuncSetAttribute(k_table_pass1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_table_pass1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_table_pass2<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_table_pass2<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  g_attr_done = true;
+  static SmemLimit l1, l2, l3, l4;
+  const size_t smem = (size_t)THREADS * K_TABLE * 8;
+  l1.raise((const void*)k_table_pass1<false>, smem);
+  l2.raise((const void*)k_table_pass1<true>, smem);
+  l3.raise((const void*)k_table_pass2<false, false>, smem);
+  l4.raise((const void*)k_table_pass2<true, false>, smem);
 }
 
 int64_t index_entries(int64_t M) {
