@@ -34,6 +34,6 @@ T = sum(tot.values()) or 1
 TI = sum(p[1] for p in per) or 1
 print(f"warp instructions {TI}, stall samples {T}")
 print("stalls:", {k: round(100 * v / T, 1) for k, v in tot.most_common(10)})
-for s, ins, ln, src, st in sorted(per, reverse=True)[:top]:
+for s, ins, ln, src, st in sorted(per, key=lambda p: (p[0], p[1]), reverse=True)[:top]:
     t3 = sorted(st.items(), key=lambda x: -x[1])[:3]
     print(f"{100*s/T:5.1f}%s {100*ins/TI:5.1f}%i L{ln:>4} {src:64s} {t3}")
