@@ -387,6 +387,14 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
     for (int i = threadIdx.x; i < len; i += THREADS) sw[i] = wt[i];
   for (int i = len + threadIdx.x; i < TS_TABLE; i += THREADS) sw[i] = 0.0;  // tile padding
   __syncthreads();
+  // U[f] by TMA as early as possible: griddepcontrol.wait blocks only the
+  // waiting thread (and returns at once unless this CTA started before the
+  // uniforms grid finished, in which case the CTA waits at its first barrier)
+  if (threadIdx.x == 0 && Nf > 0 && tmau) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
+    bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
+  }
   STAMP(0);
   // first half of a split cluster barrier: peers may store into this CTA's
   // shared memory only once every CTA of the cluster is running
@@ -435,18 +443,11 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   if (lane == 0) s_R[warp] = R;
   if (bad) s_bad = 1;
 
-  // ---- 2. this filter's sorted uniforms (after the uniforms grid completed);
-  // the copy overlaps the exchange below
-  if (Nf > 0) {
+  // ---- 2. this filter's sorted uniforms when they could not be copied by TMA
+  // (thread 0 issued the copy at the start otherwise)
+  if (Nf > 0 && !tmau) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (tmau) {
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(&baru, (uint32_t)Nf * 8u);
-        bulk_g2s(su, ut, (uint32_t)Nf * 8u, &baru);
-      }
-    } else {
-      for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = a.Uin[f * Nf + i];
-    }
+    for (int64_t i = threadIdx.x; i < Nf; i += THREADS) su[i] = a.Uin[f * Nf + i];
   }
 
   STAMP(3);
