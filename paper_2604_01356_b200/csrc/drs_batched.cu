@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(THREADS) k_batched_uniforms(const __grid_const
 constexpr int UW_FILTERS = 4;                 // warps (filters) per CTA
 constexpr int UW_BUF = TS_UNIF + 8;           // doubles per warp: Philox words, then row totals, then U
 template <int NW>  // spacing rows = ceil((N_f + 1) / 64), unrolled without guards
-__global__ void __launch_bounds__(UW_FILTERS * LANES, 6) k_batched_uniforms_warp(const __grid_constant__ BatchedArgs a,
+__global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp(const __grid_constant__ BatchedArgs a,
                                                                                 double* __restrict__ U) {
   asm volatile("griddepcontrol.launch_dependents;");  // the cluster kernel may start its weight copies
   __shared__ __align__(16) double sbuf[UW_FILTERS][UW_BUF];
@@ -314,17 +314,22 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 6) k_batched_uniforms_warp
   const double zmin = __longlong_as_double((long long)mn);
   const bool rep = !(zmin > __dmul_rn(1e-14, A));  // the exactness check of randkit.py:95
   const bool vec = (((uintptr_t)Uf) & 15) == 0;
+  // all 2 NW divisions first (independent, so they overlap), then the stores
+  double u0[NW], u1[NW];
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     const double Q = rows[w * (LANES + 1) + lane];
-    const double u0 = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc0[w])), A);
-    const double u1 = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc1[w])), A);
+    u0[w] = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc0[w])), A);
+    u1[w] = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc1[w])), A);
+  }
+#pragma unroll
+  for (int w = 0; w < NW; ++w) {
     const int e0 = 64 * w + 2 * lane;
     if (vec && e0 + 1 < Nf) {
-      *reinterpret_cast<double2*>(Uf + e0) = make_double2(u0, u1);
+      *reinterpret_cast<double2*>(Uf + e0) = make_double2(u0[w], u1[w]);
     } else {
-      if (e0 < Nf) Uf[e0] = u0;
-      if (e0 + 1 < Nf) Uf[e0 + 1] = u1;
+      if (e0 < Nf) Uf[e0] = u0[w];
+      if (e0 + 1 < Nf) Uf[e0 + 1] = u1[w];
     }
   }
   if (rep) {  // warp-uniform, rare: lane 0 checks and repairs the stored U serially
