@@ -158,6 +158,84 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
   }
 }
 
+// The throughput variant for many u's (k_match_index_sm): KQ searches per
+// thread in lock-step, and every global node is read as 72 bytes instead of
+// 128 -- its entry 7 decides the half (entries 0..7 are all < x when entry 7
+// is), then the half's 8 entries by two 256-bit loads.  The searches of the
+// c5 shape are bound by the L1 data pipe (every lane reads its own line), so
+// bytes per node, not dependent round trips, set their time.
+__device__ __forceinline__ int count_lt16_half(const double* p, double x) {
+  const double p7 = __ldg(p + 7);
+  const bool up = p7 < x;
+  const double* h = p + (up ? 8 : 0);
+  double v[8];
+  ldg256(h + 0, v[0], v[1], v[2], v[3]);
+  ldg256(h + 4, v[4], v[5], v[6], v[7]);
+  int c = up ? 8 : 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c += (v[i] < x) ? 1 : 0;
+  return c;
+}
+
+template <int KQ>
+__device__ __forceinline__ void search_half(const double* __restrict__ W, const double* __restrict__ idx,
+                                            const double* sidx, const IndexDesc& d, const SmemLevels& sl,
+                                            const double x[KQ], int64_t r[KQ]) {
+  int64_t b[KQ];
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) b[q] = 0;
+  int ktop = d.levels;
+  if (sl.tg) {  // the top guide, as in search_k_sm
+    const int32_t* Gt = reinterpret_cast<const int32_t*>(sidx + (d.toff - sl.base));
+    const double* Lk = sidx + (d.off[d.kt] - sl.base);
+    const int64_t B = (int64_t)1 << d.tshift;
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const double xb = x[q] * (double)B;
+      const int64_t bk = (xb >= (double)B) ? B : ((xb > 0.0) ? (int64_t)xb : 0);  // NaN -> 0
+      int lo = Gt[bk], hi = Gt[bk + 1];
+      while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (Lk[m] < x[q]) lo = m + 1;
+        else hi = m;
+      }
+      b[q] = lo;
+    }
+    ktop = d.kt - 1;
+  }
+  for (int k = ktop; k >= 1; --k) {
+    int c[KQ];
+    if (k >= sl.k_smem) {
+      const double* base = sidx + (d.off[k] - sl.base);
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) c[q] = count_lt16_smem(base + FANOUT * b[q], x[q]);
+    } else {
+      const double* base = idx + d.off[k];  // levels are padded to whole nodes with +inf
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) c[q] = count_lt16_half(base + FANOUT * b[q], x[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int64_t valid = d.n[k] - FANOUT * b[q];
+      if (c[q] >= valid) c[q] = (int)valid - 1;
+      b[q] = FANOUT * b[q] + c[q];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) {
+    const int64_t j0 = FANOUT * b[q];
+    const int64_t valid = d.n[0] - j0;
+    int c = 0;
+    if (valid >= FANOUT) {
+      c = count_lt16_half(W + j0, x[q]);
+    } else {
+      for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
+    }
+    if (c >= valid) c = (int)valid - 1;
+    r[q] = j0 + c;
+  }
+}
+
 // Sense-free grid barrier for a cooperative launch (all CTAs co-resident).
 __device__ __forceinline__ void grid_barrier(uint32_t* count, uint32_t* gen) {
   __syncthreads();
@@ -490,6 +568,9 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
 #ifndef DRS_MATCH_SMEM_CAP
 #define DRS_MATCH_SMEM_CAP 2048
 #endif
+#ifndef MATCH_KQ
+#define MATCH_KQ 4  // u's per thread in lock-step
+#endif
 // rng (optional, on the device): search only u[rng[0] .. rng[1]) and add
 // `shift` to the indices (a W shard of a sharded table)
 __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict__ W, const double* __restrict__ idx,
@@ -509,18 +590,20 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
-  for (int64_t base = lo + (int64_t)blockIdx.x * 2 * blockDim.x; base < hi; base += (int64_t)gridDim.x * 2 * blockDim.x) {
-    double x[K_UNIF];
-    int64_t i[K_UNIF];
+  constexpr int KQ = MATCH_KQ;
+  for (int64_t base = lo + (int64_t)blockIdx.x * KQ * blockDim.x; base < hi;
+       base += (int64_t)gridDim.x * KQ * blockDim.x) {
+    double x[KQ];
+    int64_t i[KQ];
 #pragma unroll
-    for (int h = 0; h < K_UNIF; ++h) {
+    for (int h = 0; h < KQ; ++h) {
       i[h] = base + h * blockDim.x + threadIdx.x;
       x[h] = (i[h] < hi) ? __ldg(u + i[h]) : 0.5;
     }
-    int64_t r[K_UNIF];
-    search_k_sm(W, idx, sidx, d, sl, x, r);
+    int64_t r[KQ];
+    search_half<KQ>(W, idx, sidx, d, sl, x, r);
 #pragma unroll
-    for (int h = 0; h < K_UNIF; ++h)
+    for (int h = 0; h < KQ; ++h)
       if (i[h] < hi) out[i[h]] = shift + r[h];
   }
 }
@@ -534,7 +617,7 @@ int launch_index_sm(const double* W, const double* idx, int64_t M, const double*
   const size_t smem = (size_t)sl.count * 8;
   lim.raise((const void*)k_match_index_sm, SIDX_CAP * 8);
   const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_match_index_sm, 256, smem);
-  const int64_t chunks = cdiv(N, 512);
+  const int64_t chunks = cdiv(N, 256 * MATCH_KQ);
   const int64_t grid = chunks < cap ? chunks : cap;
   launch_pdl(k_match_index_sm, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
