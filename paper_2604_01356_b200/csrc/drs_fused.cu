@@ -573,6 +573,10 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
 #endif
 // rng (optional, on the device): search only u[rng[0] .. rng[1]) and add
 // `shift` to the indices (a W shard of a sharded table)
+// THROUGHPUT: MATCH_KQ searches per thread reading half nodes (search_half),
+// for many u's per CTA; else two full-node searches per thread (search_k_sm),
+// the latency-bound case of few u's
+template <bool THROUGHPUT>
 __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict__ W, const double* __restrict__ idx,
                                                         IndexDesc d, SmemLevels sl, const double* __restrict__ u,
                                                         int64_t N, int64_t* __restrict__ out,
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
-  constexpr int KQ = MATCH_KQ;
+  constexpr int KQ = THROUGHPUT ? MATCH_KQ : K_UNIF;
   for (int64_t base = lo + (int64_t)blockIdx.x * KQ * blockDim.x; base < hi;
        base += (int64_t)gridDim.x * KQ * blockDim.x) {
     double x[KQ];
@@ -601,7 +605,8 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
       x[h] = (i[h] < hi) ? __ldg(u + i[h]) : 0.5;
     }
     int64_t r[KQ];
-    search_half<KQ>(W, idx, sidx, d, sl, x, r);
+    if constexpr (THROUGHPUT) search_half<KQ>(W, idx, sidx, d, sl, x, r);
+    else search_k_sm(W, idx, sidx, d, sl, x, r);
 #pragma unroll
     for (int h = 0; h < KQ; ++h)
       if (i[h] < hi) out[i[h]] = shift + r[h];
@@ -612,14 +617,25 @@ int launch_index_sm(const double* W, const double* idx, int64_t M, const double*
                     cudaStream_t st, const int64_t* rng, int64_t shift) {
   const IndexDesc d = make_index_desc(M);
   const SmemLevels sl = plan_smem_levels(d, DRS_MATCH_SMEM_CAP);
-  static SmemLimit lim;
-  static OccupancyCache occ;
+  static SmemLimit lim, lim_t;
+  static OccupancyCache occ, occ_t;
   const size_t smem = (size_t)sl.count * 8;
-  lim.raise((const void*)k_match_index_sm, SIDX_CAP * 8);
-  const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_match_index_sm, 256, smem);
-  const int64_t chunks = cdiv(N, 256 * MATCH_KQ);
+  lim.raise((const void*)k_match_index_sm<false>, SIDX_CAP * 8);
+  lim_t.raise((const void*)k_match_index_sm<true>, SIDX_CAP * 8);
+  const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_match_index_sm<false>, 256, smem);
+  // many u's per resident CTA: the data pipe bounds the searches (half nodes,
+  // MATCH_KQ per thread); few: the dependent round trips do (full nodes, two)
+  if (cdiv(N, 256 * K_UNIF) >= 4 * cap) {
+    const int64_t cap_t = (int64_t)drs_sm_count() * occ_t.get((const void*)k_match_index_sm<true>, 256, smem);
+    const int64_t chunks = cdiv(N, 256 * MATCH_KQ);
+    const int64_t grid = chunks < cap_t ? chunks : cap_t;
+    launch_pdl(k_match_index_sm<true>, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng,
+               shift);
+    return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+  }
+  const int64_t chunks = cdiv(N, 256 * K_UNIF);
   const int64_t grid = chunks < cap ? chunks : cap;
-  launch_pdl(k_match_index_sm, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
+  launch_pdl(k_match_index_sm<false>, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 
