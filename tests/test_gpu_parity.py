@@ -86,6 +86,30 @@ def test_exact_mode_large_random(drs, orc):
         np.testing.assert_array_equal(drs.binary_sampler(t, U.shape[0], ReplayStream(U[perm])), e[perm])
 
 
+def test_exact_mode_many_u_throughput_search(drs, orc):
+    """Millions of u's: the index search switches to its throughput variant
+    (four u's per thread, half-node reads); bit-exact against the oracle's
+    lower bounds, with exact boundaries, ties, zero runs, u = 1 and the clamp."""
+    rng = np.random.default_rng(78)
+    M, N = (1 << 22) + 5, 3_000_000
+    w = np.exp(2 * rng.standard_normal(M))
+    w[rng.random(M) < 0.3] = 0.0
+    w[-3:] = 0.0  # trailing zeros: u = 1 maps to the first index of the top run
+    W, _ = orc.port_build_table(w)
+    U = rng.random(N)
+    U[: N // 4] = rng.choice(W[W > 0], size=N // 4)  # exact boundaries
+    U[:1000] = 1.0
+    U = np.sort(U[U > 0])
+    e = orc.match("binary", W, U)
+    t = drs.WeightTable(W)
+    Ud = dev(U)
+    np.testing.assert_array_equal(drs.dac_match(Ud, t, check=False, mode="search").cpu().numpy(), e)
+    np.testing.assert_array_equal(drs.samplers._lower_bounds(t, Ud).cpu().numpy(), e)
+    # unsorted u (the binary matcher's input order)
+    perm = rng.permutation(U.shape[0])
+    np.testing.assert_array_equal(drs.samplers._lower_bounds(t, dev(U[perm])).cpu().numpy(), e[perm])
+
+
 def test_clamp_and_ties(drs):
     t = drs.WeightTable([0.25, 0.25, 0.5, 1.0, 1.0, 1.0])
     u = np.array([1e-300, 0.25, 0.2500000001, 0.5, 1.0])
@@ -285,7 +309,7 @@ def test_batched_bit_exact_vs_oracle(drs, orc):
                                      # row and tile edges, one and two tiles, many filters per SM
                                      (157, 16896, 511), (150, 2, 1), (149, 34, 5), (200, 1056, 64),
                                      (200, 1058, 63), (211, 8448, 100), (211, 8450, 300), (90, 9504, 200),
-                                     (50, 4096, 0), (400, 16000, 130)])
+                                     (50, 4096, 0), (400, 16000, 130), (160, 8448, 330), (160, 8448, 400)])
 def test_batched_shapes_vs_oracle(drs, orc, B, Mf, Nf):
     """Tile edges, odd M_f (no TMA path), several table / uniform tiles, more
     filters than resident CTAs, N_f = 0; bit-exact against the oracle."""
