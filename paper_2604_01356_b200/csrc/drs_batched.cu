@@ -239,6 +239,18 @@ __global__ void __launch_bounds__(THREADS) k_batched_uniforms(const __grid_const
 // randkit.py:95-116 runs on lane 0 when the spacing minimum asks for it.
 constexpr int UW_FILTERS = 4;                 // warps (filters) per CTA
 constexpr int UW_BUF = TS_UNIF + 8;           // doubles per warp: Philox words, then row totals, then U
+#ifdef DRS_PHASE_TIMING
+#define WSTAMP(ph)                                                                          \
+  do {                                                                                      \
+    if (lane == 0) {                                                                        \
+      unsigned long long tt_;                                                               \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt_));                              \
+      g_phase[150000 + ((int64_t)blockIdx.x * UW_FILTERS + warp) * 8 + (ph)] = tt_;        \
+    }                                                                                       \
+  } while (0)
+#else
+#define WSTAMP(ph) do {} while (0)
+#endif
 template <int NW>  // spacing rows = ceil((N_f + 1) / 64), unrolled without guards
 __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp(const __grid_constant__ BatchedArgs a,
                                                                                 double* __restrict__ U) {
@@ -247,6 +259,7 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t f = (int64_t)blockIdx.x * UW_FILTERS + warp;
   if (f >= a.B) return;
+  WSTAMP(0);
   const int64_t Nf = a.Nf, ne = Nf + 1;
   constexpr int nw = NW;
   double* buf = sbuf[warp];
@@ -254,6 +267,7 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
   const uint64_t k0 = a.keys[3 * f], k1 = a.keys[3 * f + 1], off = a.keys[3 * f + 2];
   const uint64_t b0 = off >> 2;
   const int nblk = (int)(((off + (uint64_t)Nf) >> 2) - b0 + 1);
+  WSTAMP(1);
   for (int blk = lane; blk < nblk; blk += 2 * LANES) {  // two blocks per lane in flight
     const int blk2 = blk + LANES;
     const U64x4 v = philox_block(k0, k1, b0 + (uint64_t)blk);
@@ -266,6 +280,7 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
     }
   }
   __syncwarp();
+  WSTAMP(2);
   const int a0 = (int)(off & 3);
   double sc0[NW], sc1[NW];
   unsigned long long mn = 0x7FF0000000000000ULL;
@@ -286,6 +301,7 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mn = min(mn, (unsigned long long)__shfl_xor_sync(FULL, mn, o));
+  WSTAMP(3);
   __syncwarp();  // the words are consumed: the buffer holds the row totals now
   double* rows = buf;  // [w][33]: chunk totals of row w, then their bases Q (in place)
 #pragma unroll
@@ -304,6 +320,7 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
     G[lane] = acc;
   }
   __syncwarp();
+  WSTAMP(4);
   double A = 0.0, R[NW];
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
@@ -354,6 +371,7 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
     }
   }
   if (lane == 0 && a.advance) a.keys[3 * f + 2] = off + (uint64_t)ne;  // every lane has read it
+  WSTAMP(5);
 }
 
 __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_constant__ BatchedArgs a) {
