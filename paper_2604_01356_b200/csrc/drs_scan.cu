@@ -69,63 +69,97 @@ __global__ void k_ws_init(ScanHdr* h) {
 constexpr int CHAIN_THREADS = 512;
 constexpr int64_t CHAIN_CHUNK = 16384;    // tiles staged in shared memory per round (a multiple of GROUP_TILES)
 constexpr int CHAIN_MAX_GROUPS = 8192;    // nt <= 2^18 tiles
-constexpr size_t CHAIN_SMEM = (size_t)CHAIN_CHUNK * 8 + (size_t)CHAIN_MAX_GROUPS * 8;
+constexpr size_t CHAIN_SMEM = (size_t)(CHAIN_CHUNK + CHAIN_CHUNK / 32) * 8 + (size_t)CHAIN_MAX_GROUPS * 8;
 
 __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64_t nt, int mode,
                                                                int32_t* status_out, double* total_out,
                                                                int64_t chunk) {
   extern __shared__ __align__(16) double csm[];
   pdl_wait();
+  STAMP1(0);
   pdl_trigger();  // one CTA: the next grid may take the other SMs now
-  double* sa = csm;          // [chunk] tile totals -> exclusive in-group folds
-  double* sE = csm + chunk;  // [ng] group totals -> group bases
+  // [chunk + chunk / 32] tile totals -> exclusive in-group folds, one pad slot
+  // per group of 32 so that the per-group folds (thread g reads group g) hit
+  // different banks; then [ng] group totals -> group bases
+  double* sa = csm;
+  double* sE = csm + chunk + chunk / GROUP_TILES;
   __shared__ unsigned long long s_min;
   if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
   const int64_t ng = cdiv(nt, GROUP_TILES);
   unsigned long long mn = 0x7FF0000000000000ULL;
   for (int64_t c0 = 0; c0 < nt; c0 += chunk) {
     const int64_t c1 = (c0 + chunk < nt) ? c0 + chunk : nt;
-    // 1. stage the chunk's tile totals (coalesced, all loads in flight)
-    for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) {
-      sa[t - c0] = ws.agg[t];
-      if (mode == 1) mn = min(mn, (unsigned long long)__double_as_longlong(ws.incl[t]));
+    // 1. stage the chunk's tile totals (coalesced; eight loads per thread in
+    // flight before the first store, so the staging costs one round trip per
+    // eight rather than one per tile)
+    for (int64_t tb = c0 + threadIdx.x; tb < c1; tb += 8 * CHAIN_THREADS) {
+      double v[8], m[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t t = tb + (int64_t)k * CHAIN_THREADS;
+        v[k] = (t < c1) ? __ldcg(ws.agg + t) : 0.0;
+        m[k] = (mode == 1 && t < c1) ? __ldcg(ws.incl + t) : __longlong_as_double(0x7FF0000000000000LL);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int64_t t = tb + (int64_t)k * CHAIN_THREADS;
+        if (t < c1) sa[(t - c0) + ((t - c0) >> 5)] = v[k];
+        mn = min(mn, (unsigned long long)__double_as_longlong(m[k]));
+      }
     }
     __syncthreads();
+    STAMP(1);
     // 2. one thread per group: serial left fold from shared memory
     const int64_t g0 = c0 / GROUP_TILES, g1 = cdiv(c1, GROUP_TILES);
     static_assert(CHAIN_CHUNK % GROUP_TILES == 0, "chunks hold whole groups");
     for (int64_t g = g0 + threadIdx.x; g < g1; g += CHAIN_THREADS) {
-      const int64_t t0 = g * GROUP_TILES - c0;
-      const int64_t t1 = ((g + 1) * GROUP_TILES < c1 ? (g + 1) * GROUP_TILES : c1) - c0;
+      const int64_t gl = g - g0;  // group within the chunk: its 32 tiles start at 33 gl
+      const int len = (int)(((g + 1) * GROUP_TILES < c1 ? (g + 1) * GROUP_TILES : c1) - g * GROUP_TILES);
+      double* ga = sa + gl * (GROUP_TILES + 1);
       double D = 0.0;
-      int64_t t = t0;
-      for (; t + 8 <= t1; t += 8) {
+      int t = 0;
+      for (; t + 8 <= len; t += 8) {
         double v[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = sa[t + k];
+        for (int k = 0; k < 8; ++k) v[k] = ga[t + k];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-          sa[t + k] = D;
+          ga[t + k] = D;
           D = __dadd_rn(D, v[k]);
         }
       }
-      for (; t < t1; ++t) {
-        const double v = sa[t];
-        sa[t] = D;
+      for (; t < len; ++t) {
+        const double v = ga[t];
+        ga[t] = D;
         D = __dadd_rn(D, v);
       }
       sE[g] = D;
     }
     __syncthreads();
+    STAMP(2);
     // 3. write the exclusive in-group folds back (coalesced)
-    for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) ws.incl[t] = sa[t - c0];
+    for (int64_t t = c0 + threadIdx.x; t < c1; t += CHAIN_THREADS) ws.incl[t] = sa[(t - c0) + ((t - c0) >> 5)];
     __syncthreads();
   }
+  STAMP(3);
   if (mode == 1) block_min_u64(&s_min, mn);
   __syncthreads();
   if (threadIdx.x == 0) {
+    // serial left fold of the group totals; eight loads ahead of the adds,
+    // so the chain costs one fp64 add latency per group, not a shared load
     double C = 0.0;
-    for (int64_t g = 0; g < ng; ++g) {
+    int64_t g = 0;
+    for (; g + 8 <= ng; g += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = sE[g + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        sE[g + k] = C;
+        C = __dadd_rn(C, v[k]);
+      }
+    }
+    for (; g < ng; ++g) {
       const double e = sE[g];
       sE[g] = C;
       C = __dadd_rn(C, e);
@@ -145,8 +179,16 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
     }
   }
   __syncthreads();
+  STAMP1(4);
   for (int64_t g = threadIdx.x; g < ng; g += CHAIN_THREADS) ws.grp[g] = sE[g];
+  STAMP(5);
 }
+
+#ifdef DRS_PHASE_TIMING
+extern "C" int dr_debug_phase_times_scan(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total,
                   cudaStream_t st) {
@@ -155,7 +197,7 @@ void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double
   // shared memory sized to the call (whole groups of tiles, then the group
   // totals): small chains launch without reconfiguring a 192 KB carve-out
   const int64_t chunk = std::min<int64_t>(CHAIN_CHUNK, cdiv(nt, GROUP_TILES) * GROUP_TILES);
-  const size_t smem = (size_t)(chunk + cdiv(nt, GROUP_TILES)) * 8;
+  const size_t smem = (size_t)(chunk + chunk / GROUP_TILES + cdiv(nt, GROUP_TILES)) * 8;
   launch_pdl(k_chain_groups, dim3(1), dim3(CHAIN_THREADS), smem, st, s, nt, mode, status, total, chunk);
 }
 
