@@ -122,7 +122,7 @@ constexpr int MT_UC = 1024;   // u's staged per merge-path chunk (8 KB)
 
 __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __restrict__ W, int64_t M,
                                                             const double* __restrict__ U, int64_t N,
-                                                            int64_t* __restrict__ out, int tw) {
+                                                            int64_t* __restrict__ out, int tw, int paths) {
   extern __shared__ __align__(128) double msm[];
   double* sw = msm;            // [tw]
   double* su = msm + tw;       // [MT_UC]
@@ -154,7 +154,8 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t ib = s_ib, ie = s_ie;
-  if (ie - ib <= 2 * MT_THREADS) {
+  // short u-runs (or no room for a u chunk: paths == 0): a bisection per u
+  if (!paths || ie - ib <= 2 * MT_THREADS) {
     for (int64_t i = ib + threadIdx.x; i < ie; i += MT_THREADS) {
       const double x = __ldg(U + i);
       int lo = 0, hi = len - 1;
@@ -274,10 +275,15 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
   const int sms = drs_sm_count();
   // tiles of up to 4096 entries; smaller for small tables so that every SM
   // gets >= ~6 tiles to overlap
-  int tw = MT_TW;
+  int tw = MT_TW;  // 8192 / 16384: c3 ccf 105.8 / 118.3 us against 104.8 (scripts/merge_tw_sweep.sh)
   while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
-  const size_t smem = (size_t)(tw + 2 * MT_UC) * sizeof(double);
-  launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, U, N, out, tw);
+  // when a tile holds few u's on average (M >> N) the u chunk of the merge
+  // path is not allocated: the CTA is its W tile alone, so more tiles are in
+  // flight per SM; a tile that still holds a long run bisects every u
+  const int paths = (double)N * tw >= 64.0 * (double)M ? 1 : 0;
+  const size_t smem = (size_t)(tw + (paths ? 2 * MT_UC : 0)) * sizeof(double);
+  launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, U, N, out, tw,
+             paths);
   return launch_rc();
 }
 
