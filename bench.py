@@ -212,7 +212,11 @@ def run_drs(args, rank, world, local_rank):
         graph_step = None
         fused = args.sampler == "dac" and args.mode != "merge" and M > 16 * N and (N + 1) <= 148 * 512
         # sorted uniforms = pass 1 + chain + pass 2 + finalize, then the search
-        launches_per_step = {"binary": 1, "ccf": 5}.get(args.sampler, 1 if fused else 5)
+        # (merge: k_merge_tiles, plus k_merge_heavy for the long runs when N > 4096)
+        merge_launches = 5 + (1 if N > 4096 else 0)
+        dac_merge = args.mode == "merge" or (args.mode == "auto" and M <= 16 * N)
+        launches_per_step = {"binary": 1, "ccf": merge_launches}.get(
+            args.sampler, 1 if fused else (merge_launches if dac_merge else 5))
         if args.graph:
             # the same call captured once in a CUDA graph; the stream position
             # lives on the device, so every replay draws fresh uniforms

@@ -119,6 +119,7 @@ __device__ __forceinline__ int smem_lower_bound(const double* a, int n, double x
 constexpr int MT_THREADS = 256;
 constexpr int MT_TW = 4096;   // max W entries per tile (32 KB)
 constexpr int MT_UC = 1024;   // u's staged per merge-path chunk (8 KB)
+constexpr int MT_HEAVY = 4 * MT_UC;  // a tile's u-run longer than this is spread over k_merge_heavy
 
 __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __restrict__ W, int64_t M,
                                                             const double* __restrict__ U, int64_t N,
@@ -151,25 +152,39 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
     if (lane == 0) s_ie = v;
   }
   __syncthreads();
-  pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t ib = s_ib, ie = s_ie;
+  // a long run: the whole MT_UC-chunks inside it are left to k_merge_heavy
+  // (many CTAs), each marked in out[] by the first slot of the chunk holding
+  // -1 - t; this CTA keeps the ragged ends [ib, sk0) and [sk1, ie)
+  int64_t sk0 = ie, sk1 = ie;
+  if (ie - ib > MT_HEAVY) {
+    sk0 = (ib + MT_UC - 1) / MT_UC * MT_UC;
+    sk1 = ie / MT_UC * MT_UC;
+    for (int64_t k = sk0 / MT_UC + threadIdx.x; k < sk1 / MT_UC; k += MT_THREADS) out[k * MT_UC] = -1 - t;
+  }
   // short u-runs (or no room for a u chunk: paths == 0): a bisection per u
   if (!paths || ie - ib <= 2 * MT_THREADS) {
-    for (int64_t i = ib + threadIdx.x; i < ie; i += MT_THREADS) {
-      const double x = __ldg(U + i);
-      int lo = 0, hi = len - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (sw[mid] < x) lo = mid + 1;
-        else hi = mid;
+    for (int seg = 0; seg < 2; ++seg) {
+      const int64_t r0 = seg ? sk1 : ib, r1 = seg ? ie : sk0;
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += MT_THREADS) {
+        const double x = __ldg(U + i);
+        int lo = 0, hi = len - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (sw[mid] < x) lo = mid + 1;
+          else hi = mid;
+        }
+        out[i] = j0 + lo;
       }
-      out[i] = j0 + lo;
     }
+    pdl_trigger();
     return;
   }
-  for (int64_t c0 = ib; c0 < ie; c0 += MT_UC) {
-    const int c = (int)((ie - c0) < MT_UC ? (ie - c0) : MT_UC);
+  for (int seg = 0; seg < 2; ++seg) {
+  const int64_t r0 = seg ? sk1 : ib, r1 = seg ? ie : sk0;
+  for (int64_t c0 = r0; c0 < r1; c0 += MT_UC) {
+    const int c = (int)((r1 - c0) < MT_UC ? (r1 - c0) : MT_UC);
     for (int i = threadIdx.x; i < c; i += MT_THREADS) su[i] = __ldg(U + c0 + i);
     __syncthreads();
     // the chunk's u's land in sw[wa0 .. wa1] (wa0 = lower bound of its first
@@ -207,6 +222,58 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
     // coalesced (the destination may be pinned host memory written over the link)
     for (int i = threadIdx.x; i < c; i += MT_THREADS) out[c0 + i] = so[i];
     __syncthreads();  // su / so reuse
+  }
+  }
+  // late (an early trigger: c2 45.0 us against 43.0): k_merge_heavy's CTAs
+  // would take the slots of the last tiles
+  pdl_trigger();
+}
+
+// The whole u-chunks of long runs (marked by k_merge_tiles): persistent CTAs
+// stride over the chunks, skip unmarked ones (one load), stage the marked
+// chunk's W tile by TMA (kept while consecutive chunks share it) and bisect.
+__global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __restrict__ W, int64_t M,
+                                                            const double* __restrict__ U, int64_t N,
+                                                            int64_t* __restrict__ out, int tw) {
+  extern __shared__ __align__(128) double hsw[];  // [tw]
+  __shared__ __align__(8) uint64_t bar;
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  __syncthreads();
+  uint32_t phase = 0;
+  int64_t cur = -1;
+  int len = 0;
+  for (int64_t k = blockIdx.x; k < N / MT_UC; k += gridDim.x) {
+    const int64_t m = out[k * MT_UC];
+    __syncthreads();  // every thread has read the marker before slot 0 is overwritten
+    if (m >= 0) continue;
+    const int64_t t = -1 - m;
+    const int64_t j0 = t * tw;
+    if (t != cur) {
+      len = (int)((M - j0) < tw ? (M - j0) : tw);
+      const int len_even = len & ~1;
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
+        if (len_even > 0) bulk_g2s(hsw, W + j0, (uint32_t)len_even * 8u, &bar);
+      }
+      if (threadIdx.x == 64 && (len & 1)) hsw[len - 1] = W[j0 + len - 1];
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      __syncthreads();
+      cur = t;
+    }
+    for (int64_t i = k * MT_UC + threadIdx.x; i < (k + 1) * MT_UC; i += MT_THREADS) {
+      const double x = __ldg(U + i);
+      int lo = 0, hi = len - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (hsw[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      out[i] = j0 + lo;
+    }
+    __syncthreads();  // hsw reuse
   }
 }
 
@@ -284,6 +351,13 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
   const size_t smem = (size_t)(tw + (paths ? 2 * MT_UC : 0)) * sizeof(double);
   launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, U, N, out, tw,
              paths);
+  if (N > MT_HEAVY) {  // a run can be long: the helper grid (it exits after one load per chunk otherwise)
+    static SmemLimit hl;
+    hl.raise((const void*)k_merge_heavy, (size_t)MT_TW * sizeof(double));
+    const int64_t nch = N / MT_UC;
+    const unsigned g = (unsigned)(nch < 2 * (int64_t)sms ? nch : 2 * (int64_t)sms);
+    launch_pdl(k_merge_heavy, dim3(g), dim3(MT_THREADS), (size_t)tw * sizeof(double), st, W, M, U, N, out, tw);
+  }
   return launch_rc();
 }
 

@@ -86,6 +86,34 @@ def test_exact_mode_large_random(drs, orc):
         np.testing.assert_array_equal(drs.binary_sampler(t, U.shape[0], ReplayStream(U[perm])), e[perm])
 
 
+@pytest.mark.parametrize("M,N,frac,blk", [
+    ((1 << 22) + 3, 600_000, 0.5, 3000),   # M >> N: tiles without a u chunk (bisection), split runs
+    ((1 << 20) + 7, 1 << 20, 0.6, 5000),   # M ~ N: merge path, split runs
+    (1 << 20, 70_001, 0.97, 1),            # one weight holds 97% of the mass: one run spans the u's
+    ((1 << 18) + 1, 300_000, 0.3, 20000),  # a heavy block spanning several tiles
+])
+def test_merge_heavy_runs(drs, orc, M, N, frac, blk):
+    """Tiles whose u-run is longer than MT_HEAVY: the tile CTA merges the
+    ragged ends, k_merge_heavy the whole chunks inside; bit-exact against the
+    oracle's lower bounds with exact boundaries inside the heavy block, for
+    CCF and DaC in merge mode, with ragged N."""
+    rng = np.random.default_rng(79)
+    w = np.exp(rng.standard_normal(M))
+    off = int(rng.integers(0, M - blk))
+    w[off:off + blk] = (w.sum() - w[off:off + blk].sum()) * frac / (1 - frac) / blk
+    W, _ = orc.port_build_table(w)
+    U = rng.random(N)
+    U[: N // 8] = rng.choice(W[off:off + blk], size=N // 8)  # exact boundaries in the heavy block
+    U = np.sort(U[U > 0])
+    e = orc.match("binary", W, U)
+    t = drs.WeightTable(W)
+    Ud = dev(U)
+    np.testing.assert_array_equal(drs.ccf_match(Ud, t, check=False).cpu().numpy(), e)
+    np.testing.assert_array_equal(drs.dac_match(Ud, t, check=False, mode="merge").cpu().numpy(), e)
+    # host input and result (U has ties, so the strict sortedness check is off)
+    np.testing.assert_array_equal(drs.ccf_match(U, t, check=False), e)
+
+
 def test_exact_mode_many_u_throughput_search(drs, orc):
     """Millions of u's: the index search switches to its throughput variant
     (four u's per thread, half-node reads); bit-exact against the oracle's
