@@ -241,39 +241,50 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __rest
   pdl_trigger();
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
+  __shared__ int64_t s_mark[MT_THREADS];
   uint32_t phase = 0;
   int64_t cur = -1;
   int len = 0;
-  for (int64_t k = blockIdx.x; k < N / MT_UC; k += gridDim.x) {
-    const int64_t m = out[k * MT_UC];
-    __syncthreads();  // every thread has read the marker before slot 0 is overwritten
-    if (m >= 0) continue;
-    const int64_t t = -1 - m;
-    const int64_t j0 = t * tw;
-    if (t != cur) {
-      len = (int)((M - j0) < tw ? (M - j0) : tw);
-      const int len_even = len & ~1;
-      if (threadIdx.x == 0) {
-        mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
-        if (len_even > 0) bulk_g2s(hsw, W + j0, (uint32_t)len_even * 8u, &bar);
+  const int64_t nch = N / MT_UC;
+  // the CTA's chunks are blockIdx.x + q * gridDim.x; their markers are read
+  // MT_THREADS at a time (one load per thread), then the marked ones processed
+  for (int64_t kb = blockIdx.x; kb < nch; kb += (int64_t)gridDim.x * MT_THREADS) {
+    const int64_t kk = kb + (int64_t)threadIdx.x * gridDim.x;
+    s_mark[threadIdx.x] = (kk < nch) ? out[kk * MT_UC] : 0;
+    __syncthreads();
+    for (int q = 0; q < MT_THREADS; ++q) {
+      const int64_t k = kb + (int64_t)q * gridDim.x;
+      if (k >= nch) break;
+      const int64_t m = s_mark[q];
+      if (m >= 0) continue;
+      const int64_t t = -1 - m;
+      const int64_t j0 = t * tw;
+      if (t != cur) {
+        len = (int)((M - j0) < tw ? (M - j0) : tw);
+        const int len_even = len & ~1;
+        if (threadIdx.x == 0) {
+          mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
+          if (len_even > 0) bulk_g2s(hsw, W + j0, (uint32_t)len_even * 8u, &bar);
+        }
+        if (threadIdx.x == 64 && (len & 1)) hsw[len - 1] = W[j0 + len - 1];
+        mbar_wait(&bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        cur = t;
       }
-      if (threadIdx.x == 64 && (len & 1)) hsw[len - 1] = W[j0 + len - 1];
-      mbar_wait(&bar, phase);
-      phase ^= 1u;
-      __syncthreads();
-      cur = t;
-    }
-    for (int64_t i = k * MT_UC + threadIdx.x; i < (k + 1) * MT_UC; i += MT_THREADS) {
-      const double x = __ldg(U + i);
-      int lo = 0, hi = len - 1;
-      while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (hsw[mid] < x) lo = mid + 1;
-        else hi = mid;
+      for (int64_t i = k * MT_UC + threadIdx.x; i < (k + 1) * MT_UC; i += MT_THREADS) {
+        const double x = __ldg(U + i);
+        int lo = 0, hi = len - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (hsw[mid] < x) lo = mid + 1;
+          else hi = mid;
+        }
+        out[i] = j0 + lo;
       }
-      out[i] = j0 + lo;
+      __syncthreads();  // hsw reuse
     }
-    __syncthreads();  // hsw reuse
+    __syncthreads();  // s_mark reuse
   }
 }
 
