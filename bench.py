@@ -74,23 +74,46 @@ def make_weights(cfg_name, rank=0, world=1):
         return out
     M = c["M"]
     if cfg_name == "c5":
-        a, b = M * rank // world, M * (rank + 1) // world
-        # 64 chunks of 2^24 from per-chunk generators; spike block holds 25% of the mass
-        chunk = 1 << 24
-        w = np.empty(b - a)
-        for k in range(a // chunk, (b + chunk - 1) // chunk):
-            g = np.exp(2.0 * np.random.default_rng([c["wseed"], k]).standard_normal(chunk))
-            s0, s1 = max(a, k * chunk), min(b, (k + 1) * chunk)
-            w[s0 - a:s1 - a] = g[s0 - k * chunk:s1 - k * chunk]
-        off = int(np.random.default_rng([c["wseed"], 999]).integers(0, M - 1024))
-        # expected total mass of the log-normal field is M e^2; the block gets a third of it
-        spike = M * np.exp(2.0) / 3.0 / 1024
-        lo, hi = max(a, off), min(b, off + 1024)
-        if lo < hi:
-            w[lo - a:hi - a] = spike
-        return w
+        return make_c5_weights(rank, world)
     rng = np.random.default_rng(c["wseed"])
     return np.exp(c["sigma"] * rng.standard_normal(M))
+
+
+C5_CHUNK = 1 << 24
+
+
+def make_c5_weights(rank=0, world=1):
+    """Config 5: w = exp(2 g), g ~ N(0, 1), drawn as 64 chunks of
+    2^24 (chunk k from default_rng([1005, k]) -- per-chunk generators, so a rank
+    can draw any chunk without drawing the ones before it), plus a block of
+    1024 contiguous entries at a seeded offset (default_rng([1005, 999])) set
+    to (total - block) / 3 / 1024, where total is the ACTUAL sum of the field
+    (chunk sums np.sum, added in chunk order) and block the block's own sum:
+    the block holds exactly 25% of the final mass.  Rank g of `world` gets
+    its contiguous range [g M / world, (g + 1) M / world); every rank draws
+    all chunks once to form the total (identical on every rank)."""
+    c = CONFIGS["c5"]
+    M = c["M"]
+    a, b = M * rank // world, M * (rank + 1) // world
+    off = int(np.random.default_rng([c["wseed"], 999]).integers(0, M - 1024))
+    w = np.empty(b - a)
+    total = 0.0
+    block = 0.0
+    for k in range(M // C5_CHUNK):
+        g = np.exp(2.0 * np.random.default_rng([c["wseed"], k]).standard_normal(C5_CHUNK))
+        total += float(g.sum())
+        k0, k1 = k * C5_CHUNK, (k + 1) * C5_CHUNK
+        blo, bhi = max(off, k0), min(off + 1024, k1)
+        if blo < bhi:
+            block += float(g[blo - k0:bhi - k0].sum())
+        s0, s1 = max(a, k0), min(b, k1)
+        if s0 < s1:
+            w[s0 - a:s1 - a] = g[s0 - k0:s1 - k0]
+    spike = (total - block) / 3.0 / 1024
+    lo, hi = max(a, off), min(b, off + 1024)
+    if lo < hi:
+        w[lo - a:hi - a] = spike
+    return w
 
 
 # ------------------------------------------------------------------ clocks
@@ -372,7 +395,76 @@ def run_drs(args, rank, world, local_rank):
         "steps_ms": [round(x, 5) for x in step_ms],
         "graph_replay_ms_per_step_median": graph_ms,
     }
+    if world == 1 and args.parity:
+        line["parity"] = parity_block(cfg, args.sampler, args.mode, w_host, locals().get("table"))
     return line, (alg_bytes, samples)
+
+
+# ---------------------------------------------------------- parity checker
+def parity_block(cfg, sampler, mode, w_host, table=None):
+    """The north star's device-mode correctness counters for one call of the
+    benchmarked sampler on this config (oracle/parity.py; the CHECKER, run
+    after the timed region at N = 1 on rank 0, never timed): exact-mode
+    mismatches of the reference matcher on the device's own W and U, W / U
+    ulp histograms against the reference association, u within 4 ulp and
+    within the measured drift of a boundary, index flips, unexplained flips."""
+    import time as _t
+
+    import torch
+
+    import paper_2604_01356_b200 as drs
+    from oracle import oracle as orc
+    from oracle import parity
+
+    t0 = _t.perf_counter()
+    c = CONFIGS[cfg]
+    if cfg == "c4":
+        # a bounded prefix of the bank: device W, U and indices against the
+        # oracle twin bit for bit, and against the reference association
+        Bs = 256
+        w = w_host[:Bs]
+        Mf, Nf = c["Mf"], c["Nf"]
+        streams = [drs.RngStream(c["useed"], (b,)) for b in range(Bs)]
+        keys = np.array([[s.key[0], s.key[1], s.position] for s in streams], dtype=np.uint64)
+        out, U, W = drs.resample_batched(w, Nf, streams, return_uniforms=True, return_tables=True)
+        eo, Uo, Wo, _ = orc.resample_batched(w, Nf, keys)
+        agg = {"filters": Bs, "twin_mismatches": int(np.count_nonzero(out != eo) + np.count_nonzero(U != Uo)
+                                                    + np.count_nonzero(W != Wo))}
+        keys_sum = ("exact_mismatches", "near_boundary_4ulp", "near_boundary_drift", "flips", "flips_unexplained")
+        for k in keys_sum:
+            agg[k] = 0
+        agg["W_max_ulp"] = agg["U_max_ulp"] = 0
+        for b in range(Bs):
+            draws = orc.uniforms(int(keys[b, 0]), int(keys[b, 1]), 0, Nf + 1)
+            r = parity.device_report("dac", W[b], U[b], out[b], w[b], draws)
+            for k in keys_sum:
+                agg[k] += r[k]
+            agg["W_max_ulp"] = max(agg["W_max_ulp"], r["W_max_ulp"])
+            agg["U_max_ulp"] = max(agg["U_max_ulp"], r["U_max_ulp"])
+        agg["ok"] = agg["twin_mismatches"] == 0 and agg["exact_mismatches"] == 0 and agg["flips_unexplained"] == 0
+        agg["seconds"] = _t.perf_counter() - t0
+        return agg
+    N = c["N"]
+    k0, k1 = orc.key_of(c["useed"])
+    fn = {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}[sampler]
+    kw = {"mode": mode} if sampler == "dac" else {}
+    if sampler == "binary":
+        out = fn(table, N, drs.RngStream(c["useed"]))
+        draws, Ud = orc.uniforms(k0, k1, 0, N), None
+    else:
+        U = torch.empty(N, dtype=torch.float64, device="cuda")
+        out = fn(table, N, drs.RngStream(c["useed"]), uniforms_out=U, **kw)
+        draws, Ud = orc.uniforms(k0, k1, 0, N + 1), U.cpu().numpy()
+        Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+    W = table.cum
+    Wo, _ = orc.build_table(w_host)
+    twin = int(np.count_nonzero(W != Wo)) + (int(np.count_nonzero(Ud != Uo)) if Ud is not None else 0)
+    del Wo
+    rep = parity.device_report(sampler, W, Ud, out, w_host, draws)
+    rep["twin_mismatches"] = twin  # device W / U vs the oracle's device-association twins
+    rep["ok"] = rep["ok"] and twin == 0
+    rep["seconds"] = _t.perf_counter() - t0
+    return rep
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -418,6 +510,23 @@ def cpu_baseline(cfg, sampler, seconds=10.0, threads=1):
             "ms_per_call": 1e3 * per}
 
 
+def host_info():
+    """CPU model and core counts of this host (the CPU baselines' hardware)."""
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"model": model, "os_cpu_count": os.cpu_count(), "usable_cpus": usable}
+
+
 def run_reference(args):
     threads = os.cpu_count() or 1
     cb = cpu_baseline(args.config, args.sampler, seconds=max(5.0, min(30.0, 2.0 * args.steps)), threads=threads)
@@ -430,6 +539,7 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic (seeded numpy weights); Philox draws",
         "config": {"workload": args.config, **CONFIGS[args.config], "sampler": args.sampler},
         "cpu_baseline": cb,
+        "cpu_host": host_info(),
         "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return line
@@ -446,6 +556,8 @@ def main():
     ap.add_argument("--impl", default="drs", choices=["drs", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", dest="parity", action="store_false",
+                    help="skip the device-mode parity block (oracle checker, after the timed region)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager API calls instead of CUDA-graph replays")
     args = ap.parse_args()
@@ -470,6 +582,13 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.config, args.sampler, seconds=args.cpu_seconds)
+            # the reference's other CPU paths on the same workload (north star: "next to the
+            # reference's CPU divide-and-conquer and Carpenter paths ... with the core count stated")
+            others = [] if args.config == "c4" else [s for s in ("dac", "ccf", "binary") if s != args.sampler]
+            line["cpu_baselines"] = {args.sampler: line["cpu_baseline"],
+                                     **{s: cpu_baseline(args.config, s, seconds=args.cpu_seconds / 2)
+                                        for s in others}}
+            line["cpu_host"] = host_info()
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

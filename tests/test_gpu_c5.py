@@ -1,0 +1,121 @@
+"""Parity at BASELINE config 5 full size (M = 2^30, N = 2^24) and the
+north star's device-mode boundary report at every config.
+
+Config 5 is the box-scale case: an 8 GiB table with 8 index levels and byte
+offsets above 2^32, a 25%-of-mass spike block (the long-run split of the
+merge, ``k_merge_heavy``), and N = 2^24 sorted uniforms, where the
+reference's exactness check (randkit.py:95-100) fires in most calls.
+
+Exact mode: the reference's matchers (oracle port of samplers.py:93-146) on
+the device's own W and U reproduce the device's indices bit for bit for dac
+(auto = index search, merge), ccf and binary; W and U equal the oracle's
+device-association twins bit for bit.  Device mode against the reference
+association (oracle/parity.py): every index flip lies within the measured
+W + U drift of a boundary.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from tests.helpers import boundary_query_set, enumerate_weight_tables
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c5():
+    from bench import CONFIGS, make_weights
+
+    w = make_weights("c5")
+    return w, CONFIGS["c5"]
+
+
+def test_c5_full_size_bit_exact(drs, orc, c5):
+    from oracle import parity
+
+    w, c = c5
+    M, N = c["M"], c["N"]
+    assert w.size == M
+    t = drs.build_weight_table(w)
+    W = t.cum
+    Wo, st = orc.build_table(w)
+    assert st == 0
+    np.testing.assert_array_equal(W, Wo)  # K1 at 2^30: bit-exact vs the device-association twin
+    del Wo
+    assert W[-1] == 1.0
+    k0, k1 = orc.key_of(c["useed"])
+    Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+    Wref, _ = orc.port_build_table(w)
+    U = torch.empty(N, dtype=torch.float64, device="cuda")
+    draws = orc.uniforms(k0, k1, 0, N + 1)
+    reports = {}
+    for kind, fn, kw in (("dac", drs.dac_sampler, {}), ("dac_merge", drs.dac_sampler, {"mode": "merge"}),
+                         ("ccf", drs.ccf_sampler, {})):
+        out = fn(t, N, drs.RngStream(c["useed"]), uniforms_out=U, **kw)
+        Ud = U.cpu().numpy()
+        np.testing.assert_array_equal(Ud, Uo)  # K2 at 2^24 (repair path included when it fires)
+        base = kind.split("_")[0]
+        rep = parity.device_report(base, W, Ud, out, w, draws, W_ref=Wref)
+        assert rep["exact_mismatches"] == 0, (kind, rep)
+        assert rep["flips_unexplained"] == 0, (kind, rep)
+        reports[kind] = rep
+    out = drs.binary_sampler(t, N, drs.RngStream(c["useed"]))
+    rep = parity.device_report("binary", W, None, out, w, draws[:N], W_ref=Wref)
+    assert rep["exact_mismatches"] == 0 and rep["flips_unexplained"] == 0, rep
+    # the spike block's run was drawn (k_merge_heavy path) and every index is in range
+    assert out.min() >= 0 and out.max() < M
+    print({k: (v["flips"], v["near_boundary_4ulp"], v["near_boundary_drift"]) for k, v in reports.items()})
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
+def test_boundary_report_device_mode(drs, cfg):
+    """The north star's proximity report at c1-c3: device W and U vs the
+    reference association; flips confined to the drift set; exact on the
+    device's own W and U."""
+    from bench import CONFIGS, make_weights
+    from oracle import oracle as orc
+    from oracle import parity
+
+    c = CONFIGS[cfg]
+    w = make_weights(cfg)
+    t = drs.build_weight_table(w)
+    N = c["N"]
+    k0, k1 = orc.key_of(c["useed"])
+    draws = orc.uniforms(k0, k1, 0, N + 1)
+    Wref, _ = orc.port_build_table(w)
+    U = torch.empty(N, dtype=torch.float64, device="cuda")
+    for kind, fn in (("dac", drs.dac_sampler), ("ccf", drs.ccf_sampler)):
+        out = fn(t, N, drs.RngStream(c["useed"]), uniforms_out=U)
+        rep = parity.device_report(kind, t.cum, U.cpu().numpy(), out, w, draws, W_ref=Wref)
+        assert rep["ok"], rep
+    out = drs.binary_sampler(t, N, drs.RngStream(c["useed"]))
+    rep = parity.device_report("binary", t.cum, None, out, w, draws[:N], W_ref=Wref)
+    assert rep["ok"], rep
+
+
+def test_exhaustive_tables_size8_digest(drs, golden):
+    """Every table of size <= 8 over {0, 1, 2} (9,832 tables; reference
+    tests/helpers.py:53-76): W built on the device, its boundary query set
+    matched by every GPU matcher; the SHA-256 over (W, u, indices) equals the
+    digest of the reference's own outputs (tests/golden, make_golden.py)."""
+    import hashlib
+
+    from tests.helpers import ReplayStream
+
+    h = hashlib.sha256()
+    count = 0
+    for raw in enumerate_weight_tables(8):
+        t = drs.build_weight_table(raw)
+        W = t.cum
+        u = boundary_query_set(W)
+        e = drs.dac_match(u, t)
+        for other in (drs.ccf_match(u, t), drs.dac_match(u, t, mode="merge"), drs.dac_match(u, t, mode="search"),
+                      drs.binary_sampler(t, u.shape[0], ReplayStream(u))):
+            np.testing.assert_array_equal(other, e)
+        h.update(W.tobytes())
+        h.update(u.tobytes())
+        h.update(e.astype(np.int64).tobytes())
+        count += 1
+    assert count == int(golden["exh_count"])
+    assert h.digest() == golden["exh_digest"].tobytes()
