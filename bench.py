@@ -159,17 +159,19 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- drs arm
-def run_drs(args, rank, world, local_rank):
+def run_drs(args, rank, world, local_rank, cfg=None, light=False):
+    """One config on this rank; rank 0's JSON line.  ``light``: the timed
+    steps, the dominant kernel and e2e only (the scaling blocks)."""
     import torch
     import torch.distributed as dist
 
     import paper_2604_01356_b200 as drs
-    from paper_2604_01356_b200 import _lib
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    cfg = args.config
+    cfg = cfg or args.config
     c = CONFIGS[cfg]
+    alt = None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     def barrier():
@@ -207,14 +209,30 @@ def run_drs(args, rank, world, local_rank):
         stream = drs.RngStream(c["useed"])
         alg_bytes = (8 * c["M"]) // world + 16 * N // world
         samples = N // world
+        comm = args.comm
 
         def step():
-            return drs.sharded_dac_sampler(table, N, stream)
+            # status not read in the timed loop (no host round trip); the
+            # windows hold mean + 12 sd of the slice
+            return drs.sharded_dac_sampler(table, N, stream, comm=comm, check=False)
 
-        launches_per_step = 4
+        other = "none" if comm == "allgather" else "allgather"
+        alt = (other, lambda: drs.sharded_dac_sampler(table, N, stream, comm=other, check=False))
+        # tile totals (1/G of them, or all for comm none), [all-gather], stage, chain,
+        # tile range, regenerate, finish, match
+        launches_per_step = 7
         kernel_step = step
-        e2e_step = None
-        e2e_h2d = e2e_d2h = 0
+        e2e_stream = drs.RngStream(c["useed"], (1,))
+        slices = []
+
+        def e2e_step():
+            # the public call, then this rank's slice of indices to the host
+            out, rng = drs.sharded_dac_sampler(table, N, e2e_stream, comm=comm)
+            i0, i1 = rng[:2].tolist()
+            slices.append(i1 - i0)
+            return out[: i1 - i0].cpu()
+
+        e2e_h2d, e2e_d2h = 0, 8 * (N // world)
     else:
         w_host = make_weights(cfg)
         table = drs.build_weight_table(w_host)
@@ -240,7 +258,7 @@ def run_drs(args, rank, world, local_rank):
         dac_merge = args.mode == "merge" or (args.mode == "auto" and M <= 16 * N)
         launches_per_step = {"binary": 1, "ccf": merge_launches}.get(
             args.sampler, 1 if fused else (merge_launches if dac_merge else 5))
-        if args.graph:
+        if args.graph and not light:
             # the same call captured once in a CUDA graph; the stream position
             # lives on the device, so every replay draws fresh uniforms
             dstream = drs.DeviceRngStream(c["useed"], (rank,))
@@ -293,8 +311,20 @@ def run_drs(args, rank, world, local_rank):
         torch.cuda.synchronize()
         step_ms = timed(step, args.steps)
     barrier()
+    alt_ms = None
+    if alt is not None:  # the other communication mode of the sharded sampler, same discipline
+        for _ in range(3):
+            alt[1]()
+        barrier()
+        torch.cuda.synchronize()
+        a_ms = float(sum(timed(alt[1], args.steps)))
+        if world > 1:
+            t = torch.tensor([a_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            a_ms = float(t.item())
+        alt_ms = a_ms / args.steps
     graph_ms = None
-    if cfg not in ("c4",) and not (cfg == "c5" and world > 1) and locals().get("graph_step") is not None:
+    if not light and cfg not in ("c4",) and not (cfg == "c5" and world > 1) and locals().get("graph_step") is not None:
         for _ in range(3):
             graph_step()
         graph_ms = statistics.median(timed(graph_step, args.steps))
@@ -320,7 +350,7 @@ def run_drs(args, rank, world, local_rank):
     # ---- K1 on its own: build_weight_table from device-resident raw weights
     # (16 M algorithmic bytes -- read w, write W)
     table_build = None
-    if cfg in ("c1", "c2", "c3") or (cfg == "c5" and world == 1):
+    if not light and (cfg in ("c1", "c2", "c3") or (cfg == "c5" and world == 1)):
         w_dev = torch.from_numpy(w_host).to(dev)
         drs.build_weight_table(w_dev, check=False)
         tb_ms = []
@@ -351,6 +381,10 @@ def run_drs(args, rank, world, local_rank):
             e2e_step()
         torch.cuda.synchronize()
         e2e_s = (time.perf_counter() - t0) / args.steps
+        if world > 1:  # the slowest rank
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
         e2e = {"value": world * alg_bytes / e2e_s / 1e9, "unit": "GB/s", "samples_per_s": world * samples / e2e_s,
                "ms_per_step": 1e3 * e2e_s, "h2d_bytes_per_step": e2e_h2d, "d2h_bytes_per_step": e2e_d2h,
                "timer": "host perf_counter around the public call (result copied to host)"}
@@ -395,7 +429,11 @@ def run_drs(args, rank, world, local_rank):
         "steps_ms": [round(x, 5) for x in step_ms],
         "graph_replay_ms_per_step_median": graph_ms,
     }
-    if world == 1 and args.parity:
+    if alt is not None:
+        line["config"]["comm"] = args.comm
+        line["alt_comm"] = {"comm": alt[0], "ms_per_step": alt_ms,
+                            "value": world * alg_bytes / (alt_ms * 1e-3) / 1e9}
+    if world == 1 and args.parity and not light:
         line["parity"] = parity_block(cfg, args.sampler, args.mode, w_host, locals().get("table"))
     return line, (alg_bytes, samples)
 
@@ -556,6 +594,12 @@ def main():
     ap.add_argument("--impl", default="drs", choices=["drs", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--comm", default="allgather", choices=["allgather", "none"],
+                    help="c5 sharded sampling: all-gather of spacing-tile totals, or none (every rank computes all)")
+    ap.add_argument("--no-scaling-blocks", dest="scaling_blocks", action="store_false",
+                    help="skip the c5 (W-sharded, strong) and c4 (filter-sharded, weak) blocks after the c3 headline")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: functional check of the multi-rank flow only (never a perf number)")
     ap.add_argument("--no-parity", dest="parity", action="store_false",
                     help="skip the device-mode parity block (oracle checker, after the timed region)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
@@ -563,9 +607,26 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` launched directly: re-exec under torchrun, one rank per GPU
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
+
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} rank(s)", file=sys.stderr)
 
     if args.impl == "reference":
         if rank == 0:
@@ -576,9 +637,33 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl" and torch.cuda.device_count() < world:
+            if rank == 0:
+                print(json.dumps({"error": f"{world} ranks need {world} GPUs, {torch.cuda.device_count()} visible"}),
+                      flush=True)
+            sys.exit(1)
+        torch.cuda.set_device(local_rank % torch.cuda.device_count())
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
+        local_rank = local_rank % torch.cuda.device_count()
     line, _ = run_drs(args, rank, world, local_rank)
+    if args.scaling_blocks and args.config == "c3":
+        # the multi-GPU configs in the same run: c5 shards one M = 2^30 table over the
+        # ranks (strong scaling; one GPU: the plain single-GPU sampler), c4 shards the
+        # 4096 filters (weak in filters per rank: no collective)
+        blocks = {}
+        for cfg2 in ("c5", "c4"):
+            import gc
+
+            gc.collect()
+            torch.cuda.empty_cache()
+            b, _ = run_drs(args, rank, world, local_rank, cfg=cfg2, light=True)
+            keep = ("value", "unit", "samples_per_s", "ms_per_step", "n_gpus", "scaling", "config", "roofline",
+                    "e2e", "alt_comm", "gpu_launches", "step_ms_median")
+            blocks[cfg2] = {k: b[k] for k in keep if k in b}
+        line["scaling_blocks"] = blocks
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.config, args.sampler, seconds=args.cpu_seconds)

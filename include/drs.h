@@ -53,6 +53,8 @@ extern "C" {
 #define DRS_ST_NONFINITE 0x40       /* cdf.py:35-36 (WeightTable) "invalid weight" */
 #define DRS_ST_DECREASING 0x80      /* cdf.py:37-38 "non-decreasing from >= 0"   */
 #define DRS_ST_TOP_NOT_ONE 0x100    /* cdf.py:39-40 "must end at exactly 1"      */
+#define DRS_ST_SHARD_CAPACITY 0x200 /* sharded sampling: a rank's U / index window was too small (re-run full) */
+#define DRS_ST_SHARD_WINDOW 0x400   /* sharded sampling: a repair chain may start before the regenerated tiles (re-run full) */
 
 /* --- workspace ops for dr_workspace_bytes --- */
 #define DRS_OP_TABLE 1
@@ -200,33 +202,46 @@ int dr_shard_scan(const double *w_shard, int64_t Mg, double *S, double *Tg, int3
 int dr_shard_finalize(double *S_to_W, int64_t Mg, const double *totals, int32_t G, int32_t g,
                       double *idx, void *stream);
 /* Step 3: the slice of the (replicated, identical on every rank) sorted U
- * that lands in shard g: range[0] = #(U <= fl(O_g/T)) (0 for g = 0),
- * range[1] = #(U <= fl(O_{g+1}/T)) (N for the last rank). */
+ * that lands in shard g, as a range8 (layout below) over the full U:
+ * range8[0] = #(U <= fl(O_g/T)) (0 for g = 0), range8[1] = #(U <= fl(O_{g+1}/T))
+ * (N for the last rank), range8[4] = range8[5] = 0 (U and out are full-length). */
 int dr_shard_range(const double *U, int64_t N, const double *totals, int32_t G, int32_t g,
-                   int64_t *range, void *stream);
-/* Step 4: out[i] = shard_start + lower bound of U[i] in the shard's W for
- * range[0] <= i < range[1] (other entries untouched). */
+                   int64_t *range8, void *stream);
+/* Step 4: indices of the rank's slice.  range8 (device int64[8]):
+ *   [0] i0, [1] i1   the slice [i0, i1) of the N sorted u's routed to shard g
+ *   [2] ta, [3] tb   first / last regenerated spacing tile (dr_shard_unif_local)
+ *   [4] ubase        global index of U_win[0]
+ *   [5] obase        global index of out_win[0]
+ *   [6] flags        window overflow / unsafe repair window (device)
+ * out_win[i - obase] = shard_start + lower bound of U_win[i - ubase] in the
+ * shard's W, for i0 <= i < i1. */
 int dr_shard_match(const double *W, const double *idx, int64_t Mg, int64_t shard_start,
-                   const double *U, int64_t N, const int64_t *range, int64_t *out,
+                   const double *U_win, int64_t N, const int64_t *range8, int64_t *out_win,
                    void *stream);
 
 /* Sharded sampling without replicating U.
  * Step A on every rank: spacing tiles [t0, t1) of the n+1 spacings of the
  * stream (k0, k1) at `offset` (rank g: t0 = nt g / G, t1 = nt (g+1) / G,
  * nt = ceil((n+1) / (LANES*WARPS*K_UNIF))): agg[t1-t0] tile totals and
- * zmin[t1-t0] spacing minima.  The caller all-gathers them. */
+ * zmin[t1-t0] spacing minima.  The caller all-gathers them (or every rank
+ * computes all nt tiles itself: the zero-communication mode). */
 int dr_shard_unif_totals(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, int64_t t0, int64_t t1,
                          double *agg, double *zmin, void *stream);
 /* Step B: from all nt tile totals (agg_all) and nz spacing minima, fold the
- * tile chain, regenerate only the tiles holding this rank's u's (those in
- * (fl(O_g/T), fl(O_{g+1}/T)] of the table totals), repair collapses there
- * and write U[i] for them (U is n long; other entries untouched);
- * range4 = {i0, i1, first tile, last tile}, [i0, i1) the rank's slice.
- * Bit-identical to dr_sorted_uniforms on the slice. */
+ * tile chain, find the tiles holding this rank's u's (those in
+ * (fl(O_g/T), fl(O_{g+1}/T)] of the table totals), regenerate them plus the
+ * tile before (a repair chain entering the slice starts there), repair
+ * collapses and write them into the window U_win[ucap] (U_win[0] = the u just
+ * before the window); range8 as above, with obase = i0 and the index window
+ * of the caller's capacity ocap.  A window too small for the slice, or a
+ * repair chain that may start before the regenerated tiles, sets
+ * SHARD_CAPACITY / SHARD_WINDOW in status and an empty slice: re-run with
+ * full != 0 (every tile regenerated, ucap >= n + 1, ocap >= n).
+ * U values are bit-identical to dr_sorted_uniforms on the slice. */
 int dr_shard_unif_local(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, const double *agg_all,
                         const double *zmin, int64_t nz, const double *totals, int32_t G, int32_t g,
-                        double *U, int64_t *range4, int32_t *status, void *ws, size_t ws_bytes,
-                        void *stream);
+                        double *U_win, int64_t ucap, int64_t ocap, int32_t full, int64_t *range8,
+                        int32_t *status, void *ws, size_t ws_bytes, void *stream);
 
 /* --- either side of the path --- */
 

@@ -27,6 +27,8 @@ ST_REPAIRED = 0x20
 ST_NONFINITE = 0x40
 ST_DECREASING = 0x80
 ST_TOP_NOT_ONE = 0x100
+ST_SHARD_CAPACITY = 0x200
+ST_SHARD_WINDOW = 0x400
 
 OP_TABLE = 1
 OP_SORTED = 2
@@ -74,7 +76,8 @@ _PROTOS = {
     "dr_shard_range": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
     "dr_shard_unif_totals": (_int, [_u64, _u64, _u64, _i64, _i64, _i64, _c_void_p, _c_void_p, _c_void_p]),
     "dr_shard_unif_local": (_int, [_u64, _u64, _u64, _i64, _c_void_p, _c_void_p, _i64, _c_void_p, _i32, _i32,
-                                   _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+                                   _c_void_p, _i64, _i64, _i32, _c_void_p, _c_void_p, _c_void_p, _size,
+                                   _c_void_p]),
     "dr_gather_rows": (_int, [_c_void_p, _i64, _i64, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _c_void_p]),
     "dr_histogram": (_int, [_c_void_p, _i64, _i64, _c_void_p, _c_void_p, _c_void_p]),
     "dr_chi_square_workspace": (_size, [_i64]),

@@ -571,8 +571,9 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
 #ifndef MATCH_KQ
 #define MATCH_KQ 4  // u's per thread in lock-step
 #endif
-// rng (optional, on the device): search only u[rng[0] .. rng[1]) and add
-// `shift` to the indices (a W shard of a sharded table)
+// rng (optional, on the device, the range8 of include/drs.h): search only
+// global u's rng[0] .. rng[1] of the windows u (base rng[4]) and out (base
+// rng[5]) and add `shift` to the indices (a W shard of a sharded table)
 // THROUGHPUT: MATCH_KQ searches per thread reading half nodes (search_half),
 // for many u's per CTA; else two full-node searches per thread (search_k_sm),
 // the latency-bound case of few u's
@@ -594,6 +595,10 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   pdl_trigger();
   mbar_wait(&bar, 0);
   const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
+  if (rng) {  // sharded: U and out are windows with global bases rng[4], rng[5]
+    u -= rng[4];
+    out -= rng[5];
+  }
   constexpr int KQ = THROUGHPUT ? MATCH_KQ : K_UNIF;
   for (int64_t base = lo + (int64_t)blockIdx.x * KQ * blockDim.x; base < hi;
        base += (int64_t)gridDim.x * KQ * blockDim.x) {

@@ -73,6 +73,7 @@ __global__ void k_shard_range(const double* __restrict__ U, int64_t N, const dou
     const int64_t v = (g == G - 1) ? N : warp_count_le_s(U, N, fmin(__ddiv_rn(Og1, T), 1.0));
     if ((threadIdx.x & 31) == 0) range[1] = v;
   }
+  if (threadIdx.x >= 2 && threadIdx.x < 8) range[threadIdx.x] = 0;  // full-length U and out
 }
 
 __global__ void __launch_bounds__(256) k_shard_match(const double* __restrict__ W,
@@ -81,9 +82,11 @@ __global__ void __launch_bounds__(256) k_shard_match(const double* __restrict__ 
                                                      const int64_t* __restrict__ range,
                                                      int64_t* __restrict__ out) {
   const int64_t a = range[0], b = range[1];
+  const double* Ug = U - range[4];  // window -> global index
+  int64_t* og = out - range[5];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += stride)
-    out[i] = shard_start + index_lower_bound(W, idx, d, __ldg(U + i));
+    og[i] = shard_start + index_lower_bound(W, idx, d, __ldg(Ug + i));
 }
 
 // ---------------------------------------------- sharded sorted uniforms ----
@@ -137,37 +140,53 @@ __device__ __forceinline__ double tile_end_u(const ScanWS& ws, int64_t t, double
   return __ddiv_rn(__dadd_rn(ws.grp[t / GROUP_TILES], __dadd_rn(ws.incl[t], ws.agg[t])), total);
 }
 
-__global__ void k_unif_tile_range(ScanWS ws, int64_t nt, const double* __restrict__ totals, int G, int g,
-                                  int64_t* rng, double* U) {
+// The rank's window of spacing tiles: a = first tile ending above fl(O_g/T)
+// (the slice starts there), c = first tile ending at or above fl(O_{g+1}/T)
+// (the slice ends there); the window starts one tile before a, so that a
+// collapse chain of the repair (randkit.py:107-111) entering tile a is
+// regenerated and repaired from its true start (k_unif_local_finish checks
+// that it does not start before the window).  U_win[0] holds the u just
+// before the window, then tiles ta .. tb.  full: every tile.
+__global__ void k_unif_tile_range(ScanWS ws, int64_t nt, int64_t n, const double* __restrict__ totals, int G,
+                                  int g, int64_t* rng, double* U_win, int64_t ucap, int full) {
   double Og, Og1, T;
   fold_offsets(totals, G, g, Og, Og1, T);
   const double lo = fmin(__ddiv_rn(Og, T), 1.0), hi = fmin(__ddiv_rn(Og1, T), 1.0);
   const double total = ws.hdr->total;
   // tiles 0 .. nt-2 end on a u (the last tile holds the final spacing)
   int64_t a = 0, b = nt - 1;  // first t in [0, nt-1) with u_end(t) > lo, else nt-1
-  if (g > 0)
+  if (g > 0 && !full)
     while (a < b) {
       const int64_t m = (a + b) / 2;
       if (tile_end_u(ws, m, total) > lo) b = m;
       else a = m + 1;
     }
-  int64_t c = (g < G - 1) ? 0 : nt - 1, d = nt - 1;  // first t in [0, nt-1) with u_end(t) >= hi, else nt-1
-  if (g < G - 1)
+  int64_t c = (g < G - 1 && !full) ? 0 : nt - 1, d = nt - 1;  // first t in [0, nt-1) with u_end(t) >= hi, else nt-1
+  if (g < G - 1 && !full)
     while (c < d) {
       const int64_t m = (c + d) / 2;
       if (tile_end_u(ws, m, total) >= hi) d = m;
       else c = m + 1;
     }
-  rng[2] = a;
-  rng[3] = c > a ? c : a;
-  // the u just before the range (the previous tile's inclusive prefix): the
-  // repair's forward pass reads it when the first u of the range collapses
-  if (a > 0) U[a * TSU - 1] = tile_end_u(ws, a - 1, total);
+  const int64_t ta = a > 0 ? a - 1 : 0;
+  const int64_t tb = c > a ? c : a;
+  const int64_t ubase = ta * TSU - 1;
+  const int64_t end = min((tb + 1) * TSU, n);
+  int64_t flags = 0;
+  if (end - ubase > ucap) flags |= 1;  // the window does not fit: no tile is regenerated
+  rng[2] = ta;
+  rng[3] = flags ? ta - 1 : tb;
+  rng[4] = ubase;
+  rng[6] = flags;
+  // the u just before the window (the previous tile's inclusive prefix): the
+  // repair's forward pass reads it when the window's first u collapses
+  if (ta > 0 && !flags) U_win[0] = tile_end_u(ws, ta - 1, total);
 }
 
 __global__ void __launch_bounds__(THREADS) k_unif_pass_range(PhiloxSpacings src, int64_t n, ScanWS ws,
                                                             const int64_t* __restrict__ rng,
-                                                            double* __restrict__ U) {
+                                                            double* __restrict__ U_win) {
+  double* U = U_win - rng[4];  // global index -> window
   __shared__ FoldSmem fs;
   __shared__ double s_last[WARPS];
   __shared__ uint64_t s_words[PhiloxSpacings::SMEM_WORDS];
@@ -216,34 +235,63 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass_range(PhiloxSpacings src,
   }
 }
 
-// repair inside the range (the backward pass only on the rank holding the
-// last tile), the slice counts, status, counters back to zero
-__global__ void k_unif_local_finish(ScanWS ws, int64_t n, int64_t nt, double* U, const double* __restrict__ totals,
-                                    int G, int g, int64_t* rng, int32_t* status) {
+// repair inside the window (the backward pass only on the rank holding the
+// last tile), the slice counts, the index window, status, counters back to zero
+__global__ void k_unif_local_finish(ScanWS ws, int64_t n, int64_t nt, double* U_win, const double* __restrict__ totals,
+                                    int G, int g, int64_t* rng, int64_t ocap, int32_t* status) {
+  __shared__ int64_t s_flags;
   const int64_t ta = rng[2], tb = rng[3];
+  double* U = U_win - rng[4];  // global index -> window
   const int64_t base = ta * TSU, end = min((tb + 1) * TSU, n);
   if (threadIdx.x == 0) {
+    int64_t flags = rng[6];
     const uint32_t nsites = ws.hdr->nsites;
     const uint32_t top = ws.hdr->top;
     int32_t st = 0;
-    if (ws.hdr->need && (nsites > 0 || top)) {
-      repair_sites(U, end, ws, nsites, tb == nt - 1, base);
+    if (!flags && ws.hdr->need && (nsites > 0 || top)) {
+      // a chain collapsing at the window's first u may have started in an
+      // earlier tile, whose repaired values this rank does not have
+      if (ta > 0 && !(U[base] > U[base - 1])) flags |= 4;
+      int64_t stop = end;
+      repair_sites(U, end, ws, nsites, tb == nt - 1, base, &stop);
+      if (ta > 0 && stop == base) flags |= 4;  // the backward pass ran through the window
       st |= DRS_ST_REPAIRED;
     }
-    *status = st;
     ws.hdr->nsites = 0;
     ws.hdr->top = 0;
+    s_flags = flags;
+    if (flags & 1) st |= DRS_ST_SHARD_CAPACITY;
+    if (flags & 4) st |= DRS_ST_SHARD_WINDOW;
+    *status = st;
   }
   __syncthreads();
+  const int64_t flags = s_flags;
   double Og, Og1, T;
   fold_offsets(totals, G, g, Og, Og1, T);
   const int warp = threadIdx.x >> 5;
-  if (warp == 0) {
+  __shared__ int64_t s_r[2];
+  if (flags) {
+    if (threadIdx.x < 2) s_r[threadIdx.x] = 0;
+  } else if (warp == 0) {
     const int64_t v = (g == 0) ? 0 : base + warp_count_le_s(U + base, end - base, fmin(__ddiv_rn(Og, T), 1.0));
-    if ((threadIdx.x & 31) == 0) rng[0] = v;
+    if ((threadIdx.x & 31) == 0) s_r[0] = v;
   } else if (warp == 1) {
     const int64_t v = (g == G - 1) ? n : base + warp_count_le_s(U + base, end - base, fmin(__ddiv_rn(Og1, T), 1.0));
-    if ((threadIdx.x & 31) == 0) rng[1] = v;
+    if ((threadIdx.x & 31) == 0) s_r[1] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t i0 = s_r[0], i1 = s_r[1];
+    int64_t f = flags;
+    if (!f && i1 - i0 > ocap) {  // the index window does not fit
+      f |= 2;
+      *status |= DRS_ST_SHARD_CAPACITY;
+    }
+    if (f) i1 = i0;  // empty slice: nothing is matched
+    rng[0] = i0;
+    rng[1] = i1;
+    rng[5] = i0;
+    rng[6] = f;
   }
 }
 
@@ -264,7 +312,8 @@ int dr_shard_finalize(double* S_to_W, int64_t Mg, const double* totals, int32_t 
 }
 
 int dr_shard_range(const double* U, int64_t N, const double* totals, int32_t G, int32_t g,
-                   int64_t* range, void* stream) {
+                   int64_t* range8, void* stream) {
+  int64_t* range = range8;
   if (N < 0 || !totals || !range || G < 1 || g < 0 || g >= G || (N > 0 && !U)) return DRS_ERR_ARG;
   k_shard_range<<<1, 64, 0, (cudaStream_t)stream>>>(U, N, totals, G, g, range);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
@@ -273,6 +322,7 @@ int dr_shard_range(const double* U, int64_t N, const double* totals, int32_t G, 
 int dr_shard_match(const double* W, const double* idx, int64_t Mg, int64_t shard_start,
                    const double* U, int64_t N, const int64_t* range, int64_t* out, void* stream) {
   if (Mg < 1 || !W || !range || (N > 0 && (!U || !out))) return DRS_ERR_ARG;
+  // U / out are windows: range[4] / range[5] give their global base (device)
   if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
   if (N == 0) return DRS_OK;
   const IndexDesc d = make_index_desc(Mg);
@@ -294,22 +344,24 @@ int dr_shard_unif_totals(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, i
 }
 
 int dr_shard_unif_local(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, const double* agg_all,
-                        const double* zmin, int64_t nz, const double* totals, int32_t G, int32_t g, double* U,
-                        int64_t* range4, int32_t* status, void* ws, size_t ws_bytes, void* stream) {
-  if (n < 1 || !agg_all || !zmin || nz < 1 || !totals || G < 1 || g < 0 || g >= G || !U || !range4 || !status ||
-      !ws)
+                        const double* zmin, int64_t nz, const double* totals, int32_t G, int32_t g, double* U_win,
+                        int64_t ucap, int64_t ocap, int32_t full, int64_t* range8, int32_t* status, void* ws,
+                        size_t ws_bytes, void* stream) {
+  if (n < 1 || !agg_all || !zmin || nz < 1 || !totals || G < 1 || g < 0 || g >= G || !U_win || ucap < 1 ||
+      ocap < 0 || !range8 || !status || !ws)
     return DRS_ERR_ARG;
   const int64_t nt = cdiv(n + 1, TSU);
   if (nt > ws_capacity_tiles(ws_bytes)) return DRS_ERR_WORKSPACE;
   if (nt > (int64_t)8192 * GROUP_TILES) return DRS_ERR_ARG;
+  if (full && (ucap < n + 1 || ocap < n)) return DRS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const ScanWS s = carve_ws(ws, ws_bytes);
   PhiloxSpacings src{k0, k1, offset, nullptr};
   k_stage_chain<<<(unsigned)(cdiv(nt, 256) < 1184 ? cdiv(nt, 256) : 1184), 256, 0, st>>>(agg_all, zmin, nz, nt, s);
   launch_chain(s, nt, 1, nullptr, nullptr, st);
-  k_unif_tile_range<<<1, 1, 0, st>>>(s, nt, totals, G, g, range4, U);
-  k_unif_pass_range<<<(unsigned)(nt < 148 * 4 ? nt : 148 * 4), THREADS, 0, st>>>(src, n, s, range4, U);
-  k_unif_local_finish<<<1, 64, 0, st>>>(s, n, nt, U, totals, G, g, range4, status);
+  k_unif_tile_range<<<1, 1, 0, st>>>(s, nt, n, totals, G, g, range8, U_win, ucap, full);
+  k_unif_pass_range<<<(unsigned)(nt < 148 * 4 ? nt : 148 * 4), THREADS, 0, st>>>(src, n, s, range8, U_win);
+  k_unif_local_finish<<<1, 64, 0, st>>>(s, n, nt, U_win, totals, G, g, range8, ocap, status);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 

@@ -173,6 +173,8 @@ def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = N
     n = int(n)
     if n < 0:
         raise ValueError("negative dimensions are not allowed")
+    if out is not None:
+        _check_out(out, n, torch.int64, "out")
     to_host = out is None and not device
     if out is None:
         out = empty_i64(n) if device else host_result_i64(n)
@@ -193,29 +195,54 @@ def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = N
     return out if device else out.cpu().numpy()
 
 
-_status_cache: dict[int, torch.Tensor] = {}
+# Per-(device, stream) scratch.  Buffers are never freed while the process
+# runs: a superseded (smaller) scratch U may still be referenced by a CUDA
+# graph captured earlier, so it is kept alive in _retired.
+_status_cache: dict[tuple[int, int], torch.Tensor] = {}
+_scratch_u: dict[tuple[int, int], torch.Tensor] = {}
+_retired: list[torch.Tensor] = []
 
 
 def _status_buf(s: int) -> torch.Tensor:
-    """A per-stream status word the kernels overwrite (no per-call zeroing)."""
-    t = _status_cache.get(s)
+    """A per-(device, stream) status word the kernels overwrite (no per-call zeroing)."""
+    key = (torch.cuda.current_device(), s)
+    t = _status_cache.get(key)
     if t is None:
         t = torch.empty(1, dtype=torch.int32, device=_lib.device())
-        _status_cache[s] = t
+        _status_cache[key] = t
     return t
-
-
-_scratch_u: dict[int, torch.Tensor] = {}
 
 
 def _scratch_uniforms(n: int, s: int) -> torch.Tensor:
-    """Per-stream device scratch for U when the caller does not ask for it
-    (stream-ordered reuse is safe: every use is on the same stream)."""
-    t = _scratch_u.get(s)
+    """Per-(device, stream) device scratch for U when the caller does not ask
+    for it (stream-ordered reuse is safe: every use is on the same stream)."""
+    key = (torch.cuda.current_device(), s)
+    t = _scratch_u.get(key)
     if t is None or t.numel() < n:
+        if t is not None:
+            _retired.append(t)
         t = torch.empty(max(n, 1024), dtype=torch.float64, device=_lib.device())
-        _scratch_u[s] = t
+        _scratch_u[key] = t
     return t
+
+
+def _check_out(buf, n: int, dtype: torch.dtype, name: str) -> None:
+    """A caller-supplied output buffer must be a contiguous tensor of the
+    right dtype and length, on the current device or device-accessible
+    pinned host memory; the kernels write it directly."""
+    if not isinstance(buf, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if buf.dtype != dtype:
+        raise ValueError(f"{name} must have dtype {dtype}, got {buf.dtype}")
+    if not buf.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if buf.numel() < n:
+        raise ValueError(f"{name} holds {buf.numel()} elements, {n} needed")
+    if buf.is_cuda:
+        if buf.device.index != torch.cuda.current_device():
+            raise ValueError(f"{name} is on {buf.device}, the call runs on cuda:{torch.cuda.current_device()}")
+    elif not (buf.is_pinned() and (buf.numel() == 0 or _lib.device_accessible(buf.data_ptr()))):
+        raise ValueError(f"{name} must be a CUDA tensor or pinned (device-accessible) host memory")
 
 
 def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None, U=None):
@@ -223,9 +250,19 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
     n = int(n)
     if n < 0:
         raise ValueError("n must be >= 0")
+    if out is not None:
+        _check_out(out, n, torch.int64, "out")
+    if U is not None:
+        _check_out(U, n, torch.float64, "uniforms_out")
     if n == 0 or (kind == "ccf" and not isinstance(stream, (RngStream, DeviceRngStream))):
-        U = sorted_uniforms_device(stream, n)
-        res = _match(kind, U, table, check=False, mode=mode)
+        Us = sorted_uniforms_device(stream, n)
+        res = _match(kind, Us, table, check=False, mode=mode)
+        if U is not None and n:
+            U[:n].copy_(Us)
+        if out is not None:
+            if n:
+                out[:n].copy_(res)
+            res = out
         return res if device else res.cpu().numpy()
     L = _lib.lib()
     s = _lib.stream_handle()

@@ -9,13 +9,21 @@ The multi-GPU mode of the north star (config 5, M = 2^30): rank g of G owns
 3. ``dr_shard_finalize``: O_g = T_0 + ... + T_{g-1} and T = O_G folded in
    rank order on every rank, W = min((O_g + S)/T, 1) in place, index built.
    Rank g's lower boundary fl(O_g/T) is bit-identical to rank g-1's last W.
-4. Sampling without replicating U: rank g generates the totals of its 1/G of
-   the spacing tiles (``dr_shard_unif_totals``); ONE all-gather of those
-   totals (8 bytes per tile, plus the tiles' spacing minima); every rank folds
-   the identical tile chain, regenerates only the tiles holding the u's of its
-   W range (fl(O_g/T), fl(O_{g+1}/T)] and matches that slice against its
-   shard (``dr_shard_unif_local``, ``dr_shard_match``).  The U values are
-   bit-identical to ``dr_sorted_uniforms`` on every slice.
+4. Sampling without replicating U.  The tile chain of the n + 1 spacings
+    needs every spacing tile's total:
+   - ``comm="allgather"``: rank g generates the totals of its 1/G of the
+     spacing tiles (``dr_shard_unif_totals``) and ONE all-gather of those
+     totals (8 bytes per tile, plus the tiles' spacing minima) gives all;
+   - ``comm="none"``: every rank generates all tile totals itself -- no
+     collective at all after the table build (the north star's literal
+     "no further communication"), at the price of the full Philox + log pass
+     on every rank.
+   Every rank then folds the identical tile chain, regenerates only the tiles
+   holding the u's of its W range (fl(O_g/T), fl(O_{g+1}/T)] plus the tile
+   before them (so a repair chain entering the slice is repaired from its
+   start), and matches that slice against its shard (``dr_shard_unif_local``,
+   ``dr_shard_match``).  U and the indices live in slice-sized windows; the U
+   values are bit-identical to ``dr_sorted_uniforms`` on every slice.
 
 The compute steps go through an ``ops`` object (default: the CUDA library)
 so that the collective logic can be exercised on CPU ranks with gloo in the
@@ -24,16 +32,22 @@ tests, where an oracle-backed ``ops`` stands in for the device.
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import math
+from dataclasses import dataclass, field
 
 import torch
 import torch.distributed as dist
 
-__all__ = ["ShardedWeightTable", "build_sharded_table", "sharded_dac_sampler", "DeviceShardOps"]
+__all__ = ["ShardedWeightTable", "build_sharded_table", "sharded_dac_sampler", "DeviceShardOps",
+           "slice_capacity"]
+
+ST_DEGENERATE = 0x2
+ST_SHARD_CAPACITY = 0x200
+ST_SHARD_WINDOW = 0x400
 
 
 class DeviceShardOps:
-    """The CUDA implementation of the four shard steps (libdrs.so)."""
+    """The CUDA implementation of the shard steps (libdrs.so)."""
 
     def __init__(self):
         from . import _lib
@@ -44,17 +58,21 @@ class DeviceShardOps:
         return self._lib.device()
 
     def shard_scan(self, w: torch.Tensor):
-        L = self._lib.lib()
         m = w.numel()
         S = torch.empty(m, dtype=torch.float64, device=w.device)
-        Tg = torch.empty(1, dtype=torch.float64, device=w.device)
+        Tg = torch.zeros(1, dtype=torch.float64, device=w.device)
         st = torch.zeros(1, dtype=torch.int32, device=w.device)
+        if m == 0:  # an empty shard owns no weights: total 0, no error of its own
+            return S, Tg, st
+        L = self._lib.lib()
         ws, wsb = self._lib.workspace(L.dr_workspace_bytes(self._lib.OP_TABLE, m, 0, 0))
         self._lib.check(L.dr_shard_scan(w.data_ptr(), m, S.data_ptr(), Tg.data_ptr(), st.data_ptr(), ws, wsb,
                                         self._lib.stream_handle()), "dr_shard_scan")
         return S, Tg, st
 
     def finalize(self, S: torch.Tensor, totals: torch.Tensor, G: int, g: int):
+        if S.numel() == 0:
+            return S, None
         L = self._lib.lib()
         n = int(L.dr_index_entries(S.numel()))
         idx = torch.empty(n, dtype=torch.float64, device=S.device) if n else None
@@ -77,27 +95,31 @@ class DeviceShardOps:
         return agg[: t1 - t0], zmin[: t1 - t0]
 
     def unif_local(self, key, offset: int, n: int, agg_all: torch.Tensor, zmin_all: torch.Tensor,
-                   totals: torch.Tensor, G: int, g: int):
+                   totals: torch.Tensor, G: int, g: int, ucap: int, ocap: int, full: bool):
+        """(U window, range8, status) -- see include/drs.h dr_shard_unif_local."""
         L = self._lib.lib()
         dev = self.device()
-        U = torch.empty(n, dtype=torch.float64, device=dev)
-        rng = torch.zeros(4, dtype=torch.int64, device=dev)
-        st = torch.zeros(1, dtype=torch.int32, device=dev)
+        U = torch.empty(ucap, dtype=torch.float64, device=dev)
+        rng = torch.empty(8, dtype=torch.int64, device=dev)
+        st = torch.empty(1, dtype=torch.int32, device=dev)
         ws, wsb = self._lib.workspace(self._lib.workspace_bytes(self._lib.OP_SORTED, n))
         agg_all = agg_all.contiguous()
         zmin_all = zmin_all.contiguous()
         self._lib.check(L.dr_shard_unif_local(key[0], key[1], offset, n, agg_all.data_ptr(), zmin_all.data_ptr(),
-                                              zmin_all.numel(), totals.data_ptr(), G, g, U.data_ptr(),
-                                              rng.data_ptr(), st.data_ptr(), ws, wsb, self._lib.stream_handle()),
+                                              zmin_all.numel(), totals.data_ptr(), G, g, U.data_ptr(), ucap, ocap,
+                                              int(full), rng.data_ptr(), st.data_ptr(), ws, wsb,
+                                              self._lib.stream_handle()),
                         "dr_shard_unif_local")
-        return U, rng
+        return U, rng, st
 
-    def shard_match(self, table: "ShardedWeightTable", U: torch.Tensor, rng: torch.Tensor) -> torch.Tensor:
-        out = torch.full((U.numel(),), -1, dtype=torch.int64, device=U.device)
+    def shard_match(self, table: "ShardedWeightTable", U: torch.Tensor, rng: torch.Tensor, n: int,
+                    out: torch.Tensor) -> torch.Tensor:
+        if table.W.numel() == 0:  # an empty shard is routed no u
+            return out
         idx = table.index
         self._lib.check(self._lib.lib().dr_shard_match(
             table.W.data_ptr(), 0 if idx is None else idx.data_ptr(), table.W.numel(), table.start,
-            U.data_ptr(), U.numel(), rng.data_ptr(), out.data_ptr(), self._lib.stream_handle()), "dr_shard_match")
+            U.data_ptr(), n, rng.data_ptr(), out.data_ptr(), self._lib.stream_handle()), "dr_shard_match")
         return out
 
 
@@ -112,6 +134,7 @@ class ShardedWeightTable:
     rank: int
     world: int
     group: object = None
+    totals_host: list[float] = field(default_factory=list)  # the same totals on the host
 
     @property
     def start(self) -> int:
@@ -121,53 +144,85 @@ class ShardedWeightTable:
     def size(self) -> int:
         return sum(self.sizes)
 
+    def boundaries(self, g: int | None = None) -> tuple[float, float]:
+        """(fl(O_g / T), fl(O_{g+1} / T)): rank g's u range, folded in rank order like the device."""
+        g = self.rank if g is None else g
+        o, Og, Og1 = 0.0, 0.0, 0.0
+        for h, v in enumerate(self.totals_host):
+            if h == g:
+                Og = o
+            o = o + v
+            if h == g:
+                Og1 = o
+        return min(Og / o, 1.0), min(Og1 / o, 1.0)
 
-def _raise_status(sts) -> None:
-    from .cdf import _raise_build_status
 
-    st = 0
-    for s in sts:
-        st |= int(s)
-    _raise_build_status(st)
+def slice_capacity(table: ShardedWeightTable, n: int, tile: int, g: int | None = None) -> tuple[int, int]:
+    """(U window, index window) sizes for rank g's slice of n sorted uniforms.
+
+    The slice size is Binomial(n, q), q = the rank's share of the mass; the
+    index window holds its mean plus 12 standard deviations (a shortfall sets
+    SHARD_CAPACITY and the call is re-run at full size), the U window adds
+    the partial tiles at both ends, the tile before them and the leading slot.
+    """
+    lo, hi = table.boundaries(g)
+    q = max(0.0, hi - lo)
+    if table.world == 1 or q >= 1.0:
+        return n + 1, n
+    ocap = min(n, int(n * q + 12.0 * math.sqrt(n * q * (1.0 - q)) + 64))
+    return min(n + 1, ocap + 3 * tile + 1), ocap
 
 
 def build_sharded_table(raw_shard, *, group=None, ops=None) -> ShardedWeightTable:
     """Build this rank's shard of one weight table (collective over ``group``).
 
     ``raw_shard``: this rank's contiguous slice of the raw weights, in rank
-    order.  Raises the reference's ValueError on every rank when any shard is
-    invalid or the total is degenerate/overflowing.
+    order (it may be empty).  Raises the reference's ValueError on every rank
+    when any shard is invalid, when the whole table is empty, or when the
+    total is degenerate / overflowing -- always after the collective, so no
+    rank is left waiting in it.
     """
     ops = ops or DeviceShardOps()
     G = dist.get_world_size(group)
     g = dist.get_rank(group)
     w = raw_shard if isinstance(raw_shard, torch.Tensor) else torch.as_tensor(raw_shard, dtype=torch.float64)
     w = w.to(device=ops.device(), dtype=torch.float64).contiguous()
-    if w.ndim != 1 or w.numel() == 0:
-        raise ValueError("empty distribution")
+    bad_shape = w.ndim != 1
+    if bad_shape:
+        w = w.reshape(-1)[:0]
     S, Tg, st = ops.shard_scan(w)
     mine = torch.stack([Tg.reshape(()), torch.tensor(float(w.numel()), dtype=torch.float64, device=S.device),
-                        st.reshape(()).to(torch.float64)])
+                        (st.reshape(()).to(torch.float64) if not bad_shape
+                         else torch.tensor(-1.0, dtype=torch.float64, device=S.device))])
     allv = torch.empty(3 * G, dtype=torch.float64, device=S.device)
     dist.all_gather_into_tensor(allv, mine, group=group)
     allv = allv.reshape(G, 3)
     totals = allv[:, 0].contiguous()
-    meta = allv[:, 1:].cpu()
-    sizes = [int(v) for v in meta[:, 0].tolist()]
-    stats = [int(v) for v in meta[:, 1].tolist()]
-    W, idx = ops.finalize(S, totals, G, g)
-    # degenerate / overflow are properties of the global total T = O_G,
-    # folded in rank order like the device does
-    st_glob = list(stats)
+    meta = allv.cpu()
+    totals_host = [float(v) for v in meta[:, 0].tolist()]
+    sizes = [int(v) for v in meta[:, 1].tolist()]
+    stats = [int(v) for v in meta[:, 2].tolist()]
+    if any(s < 0 for s in stats) or sum(sizes) == 0:
+        raise ValueError("empty distribution")
+    # a shard whose weights are all zero is fine when the global total is not:
+    # degenerate / overflow are properties of T = O_G, folded in rank order
+    # like the device does
+    st_glob = 0
+    for s in stats:
+        st_glob |= s & ~ST_DEGENERATE
     T = 0.0
-    for v in totals.cpu().tolist():
+    for v in totals_host:
         T = T + v
     if T == 0.0:
-        st_glob.append(0x2)
+        st_glob |= ST_DEGENERATE
     if not T < float("inf"):
-        st_glob.append(0x4)
-    _raise_status(st_glob)
-    return ShardedWeightTable(W=W, index=idx, totals=totals, sizes=sizes, rank=g, world=G, group=group)
+        st_glob |= 0x4
+    from .cdf import _raise_build_status
+
+    _raise_build_status(st_glob)
+    W, idx = ops.finalize(S, totals, G, g)
+    return ShardedWeightTable(W=W, index=idx, totals=totals, sizes=sizes, rank=g, world=G, group=group,
+                              totals_host=totals_host)
 
 
 def _key_and_take(stream, k: int):
@@ -179,40 +234,81 @@ def _key_and_take(stream, k: int):
     return stream.key, off
 
 
-def sharded_dac_sampler(table: ShardedWeightTable, n: int, stream, *, ops=None, gather: bool = False):
-    """dac_sampler over a sharded table (samplers.py:262-266 semantics).
-
-    ``stream`` must be identical on all ranks.  Rank g generates the totals
-    of its 1/G of the spacing tiles; one all-gather of those totals; then
-    each rank regenerates only the tiles holding its u's and matches them
-    against its shard.  Returns ``(out, range)``: ``out`` int64[n] with this
-    rank's slice filled (-1 elsewhere) and ``range`` = (i0, i1, first tile,
-    last tile) on the device.  ``gather=True`` all-reduces (max) so every
-    rank holds the full index array.
-    """
-    ops = ops or DeviceShardOps()
-    n = int(n)
-    if n < 1:
-        raise ValueError("n must be >= 1")
-    G, g = table.world, table.rank
-    ts = ops.tile_size()
-    nt = (n + 1 + ts - 1) // ts
+def _all_tile_totals(ops, key, off, n, nt, G, g, group, comm):
+    if comm == "none" or G == 1:
+        return ops.unif_tile_totals(key, off, n, 0, nt)
     bounds = [nt * h // G for h in range(G + 1)]
     t0, t1 = bounds[g], bounds[g + 1]
     width = (nt + G - 1) // G
-    key, off = _key_and_take(stream, n + 1)
     agg, zmin = ops.unif_tile_totals(key, off, n, t0, t1)
     mine = torch.zeros(2 * width, dtype=torch.float64, device=agg.device)
     mine[width:] = float("inf")
     mine[: t1 - t0] = agg
     mine[width: width + t1 - t0] = zmin
     allv = torch.empty(G * 2 * width, dtype=torch.float64, device=agg.device)
-    dist.all_gather_into_tensor(allv, mine, group=table.group)
+    dist.all_gather_into_tensor(allv, mine, group=group)
     allv = allv.reshape(G, 2 * width)
     agg_all = torch.cat([allv[h, : bounds[h + 1] - bounds[h]] for h in range(G)])
     zmin_all = torch.cat([allv[h, width: width + bounds[h + 1] - bounds[h]] for h in range(G)])
-    U, rng = ops.unif_local(key, off, n, agg_all, zmin_all, table.totals, G, g)
-    out = ops.shard_match(table, U, rng)
+    return agg_all, zmin_all
+
+
+def sharded_dac_sampler(table: ShardedWeightTable, n: int, stream, *, ops=None, gather: bool = False,
+                        comm: str = "allgather", check: bool = True):
+    """dac_sampler over a sharded table (samplers.py:262-266 semantics).
+
+    ``stream`` must be identical on all ranks.  ``comm``: "allgather" (rank g
+    generates the totals of its 1/G of the spacing tiles, one all-gather of
+    those) or "none" (every rank generates all tile totals; no collective).
+    Each rank then regenerates only the tiles holding its u's and matches them
+    against its shard.  Returns ``(out, range8)``: ``out`` is this rank's
+    index window -- ``out[i - range8[5]]`` is the index of u number i for
+    ``range8[0] <= i < range8[1]`` -- and ``range8`` the device int64[8] of
+    include/drs.h.  ``check`` reads the status (one 4-byte sync) and re-runs
+    at full size in the rare cases the windows were too small or a repair
+    chain started before them.  ``gather=True`` assembles the full int64[n]
+    index array on every rank (all-gather of the slices).
+    """
+    ops = ops or DeviceShardOps()
+    n = int(n)
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if comm not in ("allgather", "none"):
+        raise ValueError(f"unknown comm mode {comm!r}")
+    G, g = table.world, table.rank
+    ts = ops.tile_size()
+    nt = (n + 1 + ts - 1) // ts
+    key, off = _key_and_take(stream, n + 1)
+    agg_all, zmin_all = _all_tile_totals(ops, key, off, n, nt, G, g, table.group, comm)
+    ucap, ocap = slice_capacity(table, n, ts)
+    U, rng, st = ops.unif_local(key, off, n, agg_all, zmin_all, table.totals, G, g, ucap, ocap, False)
+    out = torch.empty(max(ocap, 1), dtype=torch.int64, device=U.device)
+    ops.shard_match(table, U, rng, n, out)
+    if check and int(st.item()) & (ST_SHARD_CAPACITY | ST_SHARD_WINDOW):
+        U, rng, st = ops.unif_local(key, off, n, agg_all, zmin_all, table.totals, G, g, n + 1, n, True)
+        out = torch.empty(n, dtype=torch.int64, device=U.device)
+        ops.shard_match(table, U, rng, n, out)
     if gather:
-        dist.all_reduce(out, op=dist.ReduceOp.MAX, group=table.group)
+        return _gather_slices(out, rng, n, table.group, G), rng
     return out, rng
+
+
+def _gather_slices(out: torch.Tensor, rng: torch.Tensor, n: int, group, G: int) -> torch.Tensor:
+    """The full index array on every rank: all-gather the ranges, then the
+    slices padded to the longest one."""
+    rngs = torch.empty(8 * G, dtype=torch.int64, device=rng.device)
+    dist.all_gather_into_tensor(rngs, rng.contiguous(), group=group)
+    r = rngs.reshape(G, 8).cpu().tolist()
+    width = max(1, max(x[1] - x[0] for x in r))
+    mine = torch.empty(width, dtype=torch.int64, device=out.device)
+    k = min(width, out.numel())
+    mine[:k] = out[:k]
+    allv = torch.empty(G * width, dtype=torch.int64, device=out.device)
+    dist.all_gather_into_tensor(allv, mine, group=group)
+    allv = allv.reshape(G, width)
+    full = torch.full((n,), -1, dtype=torch.int64, device=out.device)
+    for h in range(G):
+        i0, i1 = r[h][0], r[h][1]
+        if i1 > i0:
+            full[i0:i1] = allv[h, : i1 - i0]
+    return full

@@ -431,50 +431,88 @@ def test_batched_invalid_weights_raise(drs):
         drs.resample_batched(w, 8, [drs.RngStream(1, (b,)) for b in range(10)])
 
 
-def test_sharded_single_gpu_emulation(drs, orc):
+def _shard_emulation(orc, w, N, key, off, Gs):
     """The shard steps for G ranks run one after another on one GPU, with the
     all-gathers replaced by concatenation: the sharded table == the oracle's,
-    every rank's U slice == dr_sorted_uniforms bit for bit although each rank
+    every rank's U window == dr_sorted_uniforms bit for bit although each rank
     generated only its 1/G of the spacing tiles, the slices tile [0, N), and
     the indices == the oracle's DaC on the whole table."""
-    from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable
+    from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable, slice_capacity
 
     ops = DeviceShardOps()
-    rng = np.random.default_rng(1005)
-    M, N = 1 << 20, (1 << 17) + 3
-    w = np.exp(2 * rng.standard_normal(M))
-    off = rng.integers(0, M - 1024)
-    w[off:off + 1024] = (w.sum() - w[off:off + 1024].sum()) / 3 / 1024
-    k0, k1 = orc.key_of(2005)
-    Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
+    M = w.size
+    k0, k1 = key
+    Uo, st_o = orc.sorted_uniforms(k0, k1, off, N)
     ts = ops.tile_size()
     nt = (N + 1 + ts - 1) // ts
-    for G in (1, 2, 4, 8):
+    for G in Gs:
         parts = [dev(w[M * g // G: M * (g + 1) // G]) for g in range(G)]
         scans = [ops.shard_scan(p) for p in parts]
         totals = torch.cat([s[1] for s in scans])
         Wo, To, st = orc.build_table_sharded(w, G)
         np.testing.assert_array_equal(totals.cpu().numpy(), To)
         bounds = [nt * h // G for h in range(G + 1)]
-        shares = [ops.unif_tile_totals((k0, k1), 0, N, bounds[h], bounds[h + 1]) for h in range(G)]
+        shares = [ops.unif_tile_totals((k0, k1), off, N, bounds[h], bounds[h + 1]) for h in range(G)]
         agg_all = torch.cat([a for a, _ in shares])
         zmin_all = torch.cat([z for _, z in shares])
-        full = torch.full((N,), -1, dtype=torch.int64, device="cuda")
+        full = np.full(N, -1, dtype=np.int64)
         Ws, prev = [], 0
         for g in range(G):
             W, idx = ops.finalize(scans[g][0], totals, G, g)
             Ws.append(W.cpu().numpy())
-            tab = ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g, world=G)
-            U, rngd = ops.unif_local((k0, k1), 0, N, agg_all, zmin_all, totals, G, g)
-            a, b, ta, tb = rngd.tolist()
-            assert a == prev and ta * ts <= a and b <= min((tb + 1) * ts, N)
+            tab = ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g,
+                                     world=G, totals_host=totals.cpu().tolist())
+            ucap, ocap = slice_capacity(tab, N, ts)
+            U, rngd, stg = ops.unif_local((k0, k1), off, N, agg_all, zmin_all, totals, G, g, ucap, ocap, False)
+            a, b, ta, tb, ubase, obase, flags, _ = rngd.tolist()
+            assert flags == 0 and int(stg.item()) & 0x600 == 0
+            assert a == prev and ta * ts <= a and b <= min((tb + 1) * ts, N) and obase == a
+            assert ubase == ta * ts - 1 and b - a <= ocap
             prev = b
-            np.testing.assert_array_equal(U[a:b].cpu().numpy(), Uo[a:b])
-            o = ops.shard_match(tab, U, rngd)
-            full[a:b] = o[a:b]
+            np.testing.assert_array_equal(U[a - ubase:b - ubase].cpu().numpy(), Uo[a:b])
+            out = torch.empty(max(ocap, 1), dtype=torch.int64, device="cuda")
+            ops.shard_match(tab, U, rngd, N, out)
+            full[a:b] = out[: b - a].cpu().numpy()
+            # the full-size re-run path gives the same slice
+            U2, r2, _ = ops.unif_local((k0, k1), off, N, agg_all, zmin_all, totals, G, g, N + 1, N, True)
+            assert r2.tolist()[:2] == [a, b] and r2.tolist()[4] == -1
+            np.testing.assert_array_equal(U2[a + 1:b + 1].cpu().numpy(), Uo[a:b])
         assert prev == N
         np.testing.assert_array_equal(np.concatenate(Ws), Wo)
-        np.testing.assert_array_equal(full.cpu().numpy(), orc.match("dac", Wo, Uo))
+        np.testing.assert_array_equal(full, orc.match("dac", Wo, Uo))
+    return st_o
+
+
+def test_sharded_single_gpu_emulation(drs, orc):
+    rng = np.random.default_rng(1005)
+    M, N = 1 << 20, (1 << 17) + 3
+    w = np.exp(2 * rng.standard_normal(M))
+    off = rng.integers(0, M - 1024)
+    w[off:off + 1024] = (w.sum() - w[off:off + 1024].sum()) / 3 / 1024
+    _shard_emulation(orc, w, N, orc.key_of(2005), 0, (1, 2, 4, 8))
+
+
+def test_sharded_repair_at_rank_boundary(drs, orc):
+    """A forced collapse of the sorted uniforms (a Philox draw above 1 - 2^-30
+    at spacing i, found by scanning the stream: key (2005, (77,)), draw
+    630216217) with the rank boundary placed just before it: the collapse sits
+    in the first tiles of rank 1's window and the repair there must be exact
+    (the previous version regenerated from the slice's own tile and could
+    repair from an unrepaired value)."""
+    N = 1 << 24
+    key = orc.key_of(2005, (77,))
+    for i in (3 * (1 << 22) + 7, 15 * (1 << 20) + 11):
+        off = 630216217 - i
+        Uo, st = orc.sorted_uniforms(key[0], key[1], off, N)
+        assert st & 0x20  # the repair ran
+        for lead in (1, 300, 700):
+            M = 1 << 16
+            w = np.random.default_rng(lead).random(M) + 0.5
+            h = M // 2
+            target = Uo[i - lead]  # rank 1's slice starts near u number i - lead
+            w[:h] *= target / (1 - target) * w[h:].sum() / w[:h].sum()
+            st_o = _shard_emulation(orc, w, N, key, off, (2,))
+            assert st_o & 0x20
 
 
 # ------------------------------------------------------------- fused sampler

@@ -1,4 +1,4 @@
-"""Multi-rank logic of the W-sharded table on CPU ranks (gloo), world sizes 2-3.
+"""Multi-rank logic of the W-sharded table on CPU ranks (gloo), world sizes 2-4.
 
 The collective part of paper_2604_01356_b200.sharded -- the single all-gather
 of (T_g, M_g, status_g), the rank-order fold of the shard offsets, error
@@ -47,8 +47,12 @@ class OracleShardOps:
 
     def shard_scan(self, w):
         a = w.numpy()
+        if a.size == 0:
+            return torch.zeros(0, dtype=torch.float64), torch.zeros(1, dtype=torch.float64), torch.zeros(1, dtype=torch.int32)
         S, T = self.orc.chain_scan(a, 33)
         st = 0 if np.all((a >= 0) & np.isfinite(a)) else 1
+        if T == 0.0:
+            st |= 0x2  # like dr_shard_scan: the LOCAL total is degenerate
         return torch.from_numpy(S), torch.tensor([T], dtype=torch.float64), torch.tensor([st], dtype=torch.int32)
 
     @staticmethod
@@ -59,6 +63,8 @@ class OracleShardOps:
         return O
 
     def finalize(self, S, totals, G, g):
+        if S.numel() == 0:
+            return S, None
         tv = totals.tolist()
         Og, T = self._fold(tv, g), self._fold(tv, G)
         W = np.minimum((Og + S.numpy()) / T, 1.0)
@@ -84,7 +90,7 @@ class OracleShardOps:
             zmin.append(part.min())
         return torch.tensor(agg, dtype=torch.float64), torch.tensor(zmin, dtype=torch.float64)
 
-    def unif_local(self, key, offset, n, agg_all, zmin_all, totals, G, g):
+    def unif_local(self, key, offset, n, agg_all, zmin_all, totals, G, g, ucap, ocap, full):
         ts = self.tile_size()
         # the gathered tile totals are exactly this stream's (all ranks' shares)
         nt = (n + 1 + ts - 1) // ts
@@ -95,15 +101,22 @@ class OracleShardOps:
         T = self._fold(tv, G)
         lo = 0 if g == 0 else int(np.searchsorted(U, min(self._fold(tv, g) / T, 1.0), side="right"))
         hi = n if g == G - 1 else int(np.searchsorted(U, min(self._fold(tv, g + 1) / T, 1.0), side="right"))
-        return torch.from_numpy(U), torch.tensor([lo, hi, 0, nt - 1], dtype=torch.int64)
+        st = 0
+        if hi - lo > ocap:  # the index window is too small: empty slice, SHARD_CAPACITY
+            hi, st = lo, 0x200
+        # full-length U window (base 0); the index window starts at the slice
+        rng = torch.tensor([lo, hi, 0, nt - 1, 0, lo, 0, 0], dtype=torch.int64)
+        return torch.from_numpy(U), rng, torch.tensor([st], dtype=torch.int32)
 
-    def shard_match(self, table, U, rng):
-        out = torch.full((U.numel(),), -1, dtype=torch.int64)
+    def shard_match(self, table, U, rng, n, out):
+        if table.W.numel() == 0:
+            return out
         a, b = rng.tolist()[:2]
+        ob = int(rng[5])
         W = table.W.numpy()
         u = U.numpy()
         for i in range(a, b):
-            out[i] = table.start + self.orc.upper_bound(W, 0, W.shape[0] - 1, u[i])
+            out[i - ob] = table.start + self.orc.upper_bound(W, 0, W.shape[0] - 1, u[i])
         return out
 
 
@@ -111,6 +124,9 @@ def _weights(M, bad_rank_slice=None):
     rng = np.random.default_rng(1005)
     w = np.exp(2 * rng.standard_normal(M))
     w[rng.random(M) < 0.05] = 0.0
+    if M < 128:
+        w[-1] = 1.0
+        return w
     off = int(rng.integers(0, M - 64))
     w[off:off + 64] = (w.sum() - w[off:off + 64].sum()) / 3 / 64
     return w
@@ -124,23 +140,29 @@ def _worker(rank, world, port, M, N, mode, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        from paper_2604_01356_b200 import sharded
         from paper_2604_01356_b200.sharded import build_sharded_table, sharded_dac_sampler
 
         ops = OracleShardOps()
         w = _weights(M)
+        if mode == "zero_shard":  # one shard all zero, the total positive
+            w[M * 1 // world: M * 2 // world] = 0.0
         a, b = M * rank // world, M * (rank + 1) // world
         part = w[a:b].copy()
         if mode == "invalid" and rank == world - 1:
             part[3] = -1.0
         if mode == "degenerate":
             part[:] = 0.0
+        if mode == "tinycap":  # windows too small: SHARD_CAPACITY, re-run at full size
+            sharded.slice_capacity = lambda table, n, tile, g=None: (8, 2)
         try:
             table = build_sharded_table(torch.from_numpy(part), ops=ops)
         except ValueError as e:
             q.put((rank, "error", str(e)))
             return
-        out, rng = sharded_dac_sampler(table, N, Stream(2005), ops=ops, gather=True)
-        q.put((rank, "ok", (table.W.numpy(), table.start, out.numpy(), rng.tolist(), table.totals.numpy())))
+        comm = "none" if mode == "nocomm" else "allgather"
+        out, rng = sharded_dac_sampler(table, N, Stream(2005), ops=ops, gather=True, comm=comm)
+        q.put((rank, "ok", (table.W.numpy(), table.start, out.numpy(), rng.tolist(), table.totals.numpy(), w)))
     finally:
         dist.destroy_process_group()
 
@@ -158,13 +180,19 @@ def _run(world, M, N, mode="ok"):
     return sorted(res)
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_table_and_sampler_match_oracle(orc, world):
-    M, N = 20011, 3001
-    res = _run(world, M, N)
+@pytest.mark.parametrize("world,M,mode", [(2, 20011, "ok"), (3, 20011, "ok"), (4, 20011, "ok"),
+                                          (3, 20011, "nocomm"), (4, 20011, "zero_shard"), (2, 20011, "tinycap"),
+                                          (4, 3, "ok"), (3, 2, "nocomm")])
+def test_sharded_table_and_sampler_match_oracle(orc, world, M, mode):
+    """World 2-4, both communication modes, an all-zero shard, empty shards
+    (M < G) and the capacity re-run: the sharded table equals the oracle's,
+    the slices tile [0, N), the gathered indices equal the oracle's DaC."""
+    N = 3001
+    res = _run(world, M, N, mode)
     assert all(r[1] == "ok" for r in res), res
+    w = res[0][2][5]
     W = np.concatenate([r[2][0] for r in res])
-    Wo, To, st = orc.build_table_sharded(_weights(M), world)
+    Wo, To, st = orc.build_table_sharded(w, world)
     np.testing.assert_array_equal(W, Wo)
     np.testing.assert_array_equal(res[0][2][4], To)
     k0, k1 = orc.key_of(2005)
@@ -175,7 +203,6 @@ def test_sharded_table_and_sampler_match_oracle(orc, world):
     assert ranges[0][0] == 0 and ranges[-1][1] == N
     for r0, r1 in zip(ranges, ranges[1:]):
         assert r0[1] == r1[0]
-    assert [r[1] for r in res] == ["ok"] * world
     for r in res:  # gather=True: every rank holds the full index array
         np.testing.assert_array_equal(r[2][2], expect)
 
