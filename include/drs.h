@@ -263,6 +263,14 @@ size_t dr_chi_square_workspace(int64_t M);
 int dr_chi_square(const uint64_t *counts, const double *W, int64_t M, int64_t n, double *out, void *ws,
                   size_t ws_bytes, void *stream);
 
+/* OpStats of the reference's instrumented twins (samplers.py:40-46,
+ * 178-188, 213-232, 249-252), computed exactly from a finished match:
+ * kind 0 dac, 1 ccf, 2 binary; u[N] the matched uniforms (sorted for dac /
+ * ccf, draw order for binary) and out[N] their lower bounds in W[M].
+ * counts[3] (device, zeroed here) = {comparisons, probes, max_depth}. */
+int dr_op_counts(int32_t kind, const double *W, int64_t M, const double *u, int64_t N, const int64_t *out,
+                 uint64_t *counts, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

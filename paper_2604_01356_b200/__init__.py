@@ -26,7 +26,7 @@ from .samplers import (
     warm_kernels,
 )
 from .sharded import ShardedWeightTable, build_sharded_table, sharded_dac_sampler
-from .verify import chi_square_statistic, gather_states, histogram, verify_statistics
+from .verify import chi_square_statistic, gather_states, histogram, verify_complexity, verify_statistics
 
 __all__ = [
     "RngStream",
@@ -54,6 +54,7 @@ __all__ = [
     "histogram",
     "chi_square_statistic",
     "verify_statistics",
+    "verify_complexity",
 ]
 
 __version__ = "0.1.0"

@@ -82,6 +82,7 @@ _PROTOS = {
     "dr_histogram": (_int, [_c_void_p, _i64, _i64, _c_void_p, _c_void_p, _c_void_p]),
     "dr_chi_square_workspace": (_size, [_i64]),
     "dr_chi_square": (_int, [_c_void_p, _c_void_p, _i64, _i64, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_op_counts": (_int, [_i32, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p]),
     "dr_shard_match": (_int, [_c_void_p, _c_void_p, _i64, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p]),
 }
 

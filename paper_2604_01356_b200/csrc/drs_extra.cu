@@ -86,6 +86,82 @@ __global__ void k_chi_final(const double* __restrict__ partial, int nb, double* 
   *out = s;
 }
 
+// ---------------------------------------------------------- op counts ----
+// The reference's OpStats for its instrumented CPU twins (samplers.py:40-46,
+// 178-188, 213-232, 249-252; cdf.py:116-125), reproduced EXACTLY from the
+// device result: every count is a function of W, u and the lower bounds.
+//   ccf     comparisons = out[n-1] + n (the cursor advances to out[n-1], one
+//           closing comparison per u: samplers.py:178-186);
+//   binary  probes = sum over u of the bisection steps of upper_bound_search
+//           on [0, M-1] (samplers.py:249-252);
+//   dac     the work list of _dac_instrumented visits the implicit median
+//           tree of [0, n-1]; the scope of median m is [a_u, b_u] (its tree
+//           node) with W range [out[a_u-1] or 0, out[b_u+1] or M-1] (each
+//           bound is an ancestor's match), m is visited iff its parent's W
+//           range is not a single index (else the parent filled it), and a
+//           visited m costs the bisection steps over its W range (0 when the
+//           range is one index); max_depth = the deepest visited node.
+// counts[0] comparisons, [1] probes, [2] max_depth (accumulated with atomics).
+__device__ __forceinline__ unsigned long long bisect_probes(const double* __restrict__ W, int64_t a, int64_t b,
+                                                            double x) {
+  unsigned long long p = 0;
+  while (a != b) {
+    const int64_t m = (a + b) >> 1;  // floor((a + b) / 2) for a, b >= 0
+    ++p;
+    if (__ldg(W + m) < x) a = m + 1;
+    else b = m;
+  }
+  return p;
+}
+
+__global__ void __launch_bounds__(256) k_op_counts(int kind, const double* __restrict__ W, int64_t M,
+                                                   const double* __restrict__ u, int64_t n,
+                                                   const int64_t* __restrict__ out,
+                                                   unsigned long long* counts) {
+  unsigned long long probes = 0, depth = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += stride) {
+    if (kind == 2) {  // binary
+      probes += bisect_probes(W, 0, M - 1, __ldg(u + m));
+      continue;
+    }
+    // the node of median m in the tree of [0, n-1], and its parent's scope
+    int64_t a = 0, b = n - 1, pa = -1, pb = -1;
+    unsigned long long d = 1;
+    while (true) {
+      const int64_t mid = (a + b) >> 1;
+      if (mid == m) break;
+      pa = a;
+      pb = b;
+      if (m < mid) b = mid - 1;
+      else a = mid + 1;
+      ++d;
+    }
+    if (pa >= 0) {  // visited only when the parent's W range was not one index
+      const int64_t paw = pa > 0 ? __ldg(out + pa - 1) : 0;
+      const int64_t pbw = pb < n - 1 ? __ldg(out + pb + 1) : M - 1;
+      if (paw == pbw) continue;
+    }
+    const int64_t aw = a > 0 ? __ldg(out + a - 1) : 0;
+    const int64_t bw = b < n - 1 ? __ldg(out + b + 1) : M - 1;
+    probes += bisect_probes(W, aw, bw, __ldg(u + m));
+    depth = d > depth ? d : depth;
+  }
+  // warp reduce, one atomic per warp
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    probes += __shfl_xor_sync(FULL, probes, o);
+    const unsigned long long od = __shfl_xor_sync(FULL, depth, o);
+    depth = od > depth ? od : depth;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (probes) atomicAdd(counts + 1, probes);
+    if (depth) atomicMax(counts + 2, depth);
+  }
+  if (kind == 1 && blockIdx.x == 0 && threadIdx.x == 0 && n > 0)
+    atomicAdd(counts + 0, (unsigned long long)__ldg(out + n - 1) + (unsigned long long)n);
+}
+
 }  // namespace drs
 
 using namespace drs;
@@ -133,6 +209,17 @@ int dr_chi_square(const uint64_t* counts, const double* W, int64_t M, int64_t n,
   const int nb = (int)(cdiv(M, 4096) < 1024 ? cdiv(M, 4096) : 1024);
   k_chi_partial<<<nb, CHI_THREADS, 0, st>>>((const unsigned long long*)counts, W, M, (double)n, (double*)ws);
   k_chi_final<<<1, 1, 0, st>>>((const double*)ws, nb, out);
+  return launch_rc_x();
+}
+
+int dr_op_counts(int32_t kind, const double* W, int64_t M, const double* u, int64_t N, const int64_t* out,
+                 uint64_t* counts, void* stream) {
+  if (kind < 0 || kind > 2 || M < 1 || N < 0 || !W || !counts || (N > 0 && (!u || !out))) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemsetAsync(counts, 0, 3 * sizeof(uint64_t), st) != cudaSuccess) return DRS_ERR_LAUNCH;
+  if (N == 0) return DRS_OK;
+  const int64_t blocks = cdiv(N, 256) < 148 * 8 ? cdiv(N, 256) : 148 * 8;
+  k_op_counts<<<(unsigned)blocks, 256, 0, st>>>(kind, W, M, u, N, out, (unsigned long long*)counts);
   return launch_rc_x();
 }
 

@@ -11,9 +11,10 @@ Host inputs (lists, numpy) give numpy results, CUDA-tensor inputs give CUDA
 tensors; samplers return numpy unless ``device=True``.  Every index is the
 unique lower bound ``min{j : W[j] >= u}`` computed on the device -- the
 samplers differ in search strategy only, exactly as in the reference.
-``stats=`` (operation counting, a CPU-instrumentation feature) is supported
-by ``upper_bound_search`` and ``linear_oracle``; the matchers and samplers
-raise NotImplementedError for it rather than falling back to the CPU.
+``stats=`` (an :class:`OpStats`) receives the reference's instrumented
+operation counts -- comparisons, probes, max_depth of the CPU algorithms
+(samplers.py:178-188, 213-232, 249-252) -- computed exactly on the device
+from the table, the uniforms and the indices (``dr_op_counts``).
 """
 
 from __future__ import annotations
@@ -57,12 +58,24 @@ class OpStats:
     max_depth: int = 0    # deepest divide-and-conquer scope nesting
 
 
-def _no_stats(stats, name):
-    if stats is not None:
-        raise NotImplementedError(
-            f"{name}(stats=...) counts CPU operations of the reference's instrumented "
-            "twin; the GPU path does not count and never falls back to the CPU"
-        )
+_OP_KIND = {"dac": 0, "ccf": 1, "binary": 2}
+
+
+def _op_counts(kind: str, table: WeightTable, ud: torch.Tensor, out: torch.Tensor, stats) -> None:
+    """Add the reference's instrumented operation counts for this match to
+    ``stats`` (samplers.py:178-188, 213-232, 249-252): computed exactly on the
+    device from W, the uniforms and the lower bounds (``dr_op_counts``)."""
+    n = ud.numel()
+    counts = torch.zeros(3, dtype=torch.int64, device=_lib.device())
+    if n:
+        _lib.check(_lib.lib().dr_op_counts(_OP_KIND[kind], table.device_cum.data_ptr(), table.size, ud.data_ptr(),
+                                           n, out.data_ptr(), counts.data_ptr(), _lib.stream_handle()),
+                   "dr_op_counts")
+    c, p, d = (int(v) for v in counts.cpu().tolist())
+    stats.comparisons += c
+    stats.probes += p
+    if d > stats.max_depth:
+        stats.max_depth = d
 
 
 def _lower_bounds(table: WeightTable, u: torch.Tensor) -> torch.Tensor:
@@ -112,7 +125,7 @@ def _check_sorted_open(u: torch.Tensor) -> None:
         raise ValueError("input not sorted")
 
 
-def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto"):
+def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto", stats=None):
     host = not is_device_tensor(u)
     ud, _ = to_device_f64(u)
     if ud.ndim != 1:
@@ -131,6 +144,8 @@ def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto"):
             rc = L.dr_match_dac(W.data_ptr(), _ptr(table.device_index), table.size, ud.data_ptr(), n,
                                 out.data_ptr(), _lib.DAC_MODES[mode], s)
         _lib.check(rc, f"dr_match_{kind}")
+    if stats is not None:
+        _op_counts(kind, table, ud, out, stats)
     return finish_host(out) if host else out
 
 
@@ -140,8 +155,7 @@ def ccf_match(u, table: WeightTable, stats: OpStats | None = None, check: bool =
     The table is read once, tile by tile (TMA bulk copies into shared
     memory); each tile merges with the slice of u that lands in it.
     """
-    _no_stats(stats, "ccf_match")
-    return _match("ccf", u, table, check)
+    return _match("ccf", u, table, check, stats=stats)
 
 
 def dac_match(u, table: WeightTable, stats: OpStats | None = None, check: bool = True,
@@ -152,10 +166,9 @@ def dac_match(u, table: WeightTable, stats: OpStats | None = None, check: bool =
     all of W); "search" splits by index blocks and bisects per u (reads
     O(N log(M/N)) lines); "auto" picks merge when M <= 16 N.
     """
-    _no_stats(stats, "dac_match")
     if mode not in _lib.DAC_MODES:
         raise ValueError(f"unknown mode {mode!r}")
-    return _match("dac", u, table, check, mode)
+    return _match("dac", u, table, check, mode, stats=stats)
 
 
 def _stream_args(stream, n_draws):
@@ -169,12 +182,22 @@ def _stream_args(stream, n_draws):
 def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = None,
                    *, device: bool = False, out=None):
     """n independent draws, each by a full-range search; draw order kept (samplers.py:238-252)."""
-    _no_stats(stats, "binary_sampler")
     n = int(n)
     if n < 0:
         raise ValueError("negative dimensions are not allowed")
     if out is not None:
         _check_out(out, n, torch.int64, "out")
+    if stats is not None:
+        # instrumented: the draws are materialised so their probes can be counted
+        res = empty_i64(0)
+        if n:
+            us = _draw_uniforms(stream, n)
+            res = _lower_bounds(table, us)
+            _op_counts("binary", table, us, res, stats)
+        if out is not None:
+            out[:n].copy_(res)
+            res = out
+        return res if device else res.cpu().numpy()
     to_host = out is None and not device
     if out is None:
         out = empty_i64(n) if device else host_result_i64(n)
@@ -245,8 +268,21 @@ def _check_out(buf, n: int, dtype: torch.dtype, name: str) -> None:
         raise ValueError(f"{name} must be a CUDA tensor or pinned (device-accessible) host memory")
 
 
+def _draw_uniforms(stream, n: int) -> torch.Tensor:
+    """The next n uniforms of a stream, on the device (the stream advances by n)."""
+    if isinstance(stream, RngStream):
+        return stream.uniforms_device(n)
+    if isinstance(stream, DeviceRngStream):
+        pos = stream.position
+        u = torch.empty(n, dtype=torch.float64, device=_lib.device())
+        _lib.check(_lib.lib().dr_uniforms(stream.key[0], stream.key[1], pos, n, u.data_ptr(), _lib.stream_handle()),
+                   "dr_uniforms")
+        stream.offset_tensor += n
+        return u
+    return to_device_f64(stream.uniforms(n))[0]
+
+
 def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None, U=None):
-    _no_stats(stats, f"{kind}_sampler")
     n = int(n)
     if n < 0:
         raise ValueError("n must be >= 0")
@@ -254,9 +290,16 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
         _check_out(out, n, torch.int64, "out")
     if U is not None:
         _check_out(U, n, torch.float64, "uniforms_out")
-    if n == 0 or (kind == "ccf" and not isinstance(stream, (RngStream, DeviceRngStream))):
-        Us = sorted_uniforms_device(stream, n)
-        res = _match(kind, Us, table, check=False, mode=mode)
+    if n == 0 or stats is not None or (kind == "ccf" and not isinstance(stream, (RngStream, DeviceRngStream))):
+        if isinstance(stream, DeviceRngStream):  # the instrumented path draws from the host position
+            pos = stream.position
+            hs = RngStream(stream.seed, stream._spawn_key)
+            hs._take(pos)
+            Us = sorted_uniforms_device(hs, n)
+            stream.offset_tensor += n + 1 if n else 0
+        else:
+            Us = sorted_uniforms_device(stream, n)
+        res = _match(kind, Us, table, check=False, mode=mode, stats=stats)
         if U is not None and n:
             U[:n].copy_(Us)
         if out is not None:

@@ -6,13 +6,17 @@
 * ``chi_square_statistic`` / ``verify_statistics``: the reference's Pearson
   goodness of fit (bench.py:221-246) with the counting and the statistic on
   the device; the draws come from the GPU samplers.
+* ``verify_complexity``: the reference's operation budgets (bench.py:249-310)
+  on the OpStats the GPU samplers report (``dr_op_counts``: the reference's
+  instrumented counts, computed exactly from the device's result).
 
 There is no CPU fallback: every step is a ``libdrs.so`` kernel.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import math
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -21,10 +25,10 @@ from . import _lib
 from ._tensors import is_device_tensor, read_status, status_word, to_device_f64
 from .cdf import WeightTable, build_weight_table
 from .randkit import RngStream
-from .samplers import binary_sampler, ccf_sampler, dac_sampler
+from .samplers import OpStats, binary_sampler, ccf_sampler, dac_sampler
 
 __all__ = ["gather_states", "histogram", "chi_square_statistic", "GofReport", "verify_statistics",
-           "dirichlet_uniform", "SAMPLER_ORDER"]
+           "ComplexityCell", "verify_complexity", "dirichlet_uniform", "SAMPLER_ORDER"]
 
 SAMPLER_ORDER = ("dac", "ccf", "binary")  # bench.py:41
 _SAMPLERS = {"dac": dac_sampler, "ccf": ccf_sampler, "binary": binary_sampler}
@@ -127,3 +131,84 @@ def verify_statistics(seed: int = 0, m: int = 16, n_draws: int = 1_000_000,
         stat = chi_square_statistic(counts, table, n_draws)
         reports.append(GofReport(name, m, n_draws, stat, m - 1, stat < critical))
     return reports
+
+
+@dataclass
+class ComplexityCell:
+    """Instrumented operation counts for one (N, ratio) cell vs their budgets (bench.py:103-124)."""
+
+    n: int
+    ratio: int
+    m: int
+    trials: int
+    ccf_max_comparisons: int
+    ccf_budget: int
+    binary_max_probes: int
+    dac_max_probes: int
+    probe_budget: int
+    dac_max_depth: int
+    depth_budget: int
+    dac_mean_probes: float
+    dac_mean_budget: float
+    violations: list[str] = field(default_factory=list)
+
+    @property
+    def ok(self) -> bool:
+        return not self.violations
+
+
+def verify_complexity(seed: int = 0, ns: tuple[int, ...] = (100, 1000), ratios: tuple[int, ...] = (1, 100, 1000),
+                      trials: int = 50) -> list[ComplexityCell]:
+    """bench.py:249-310 on the GPU samplers: equal-weight tables, per-sampler
+    substreams, the hard budgets per run (CCF comparisons <= N + M - 1;
+    binary and DaC probes <= N (ceil(log2 M) + 1); scope nesting <=
+    ceil(log2 N) + 1) and the statistical one per cell (mean DaC probes <=
+    4N (1 + log2(M/N + 1))), on the counts ``stats=`` reports."""
+    root = RngStream(seed)
+    cells = []
+    cell_key = 0
+    for n in ns:
+        for ratio in ratios:
+            cell_key += 1
+            m = n * ratio
+            table = build_weight_table(np.full(m, 1.0 / m))
+            streams = {name: root.substream(cell_key).substream(k) for k, name in enumerate(SAMPLER_ORDER)}
+            probe_budget = n * (math.ceil(math.log2(m)) + 1) if m > 1 else n
+            ccf_budget = n + m - 1
+            depth_budget = math.ceil(math.log2(n)) + 1 if n > 1 else 1
+            dac_mean_budget = 4.0 * n * (1.0 + math.log2(m / n + 1.0))
+            ccf_max = bin_max = dac_max = depth_max = 0
+            dac_probes = []
+            violations = []
+            for _ in range(trials):
+                s = OpStats()
+                ccf_sampler(table, n, streams["ccf"], stats=s, device=True)
+                ccf_max = max(ccf_max, s.comparisons)
+                if s.comparisons > ccf_budget:
+                    violations.append(f"ccf comparisons {s.comparisons} > {ccf_budget}")
+                s = OpStats()
+                binary_sampler(table, n, streams["binary"], stats=s, device=True)
+                bin_max = max(bin_max, s.probes)
+                if s.probes > probe_budget:
+                    violations.append(f"binary probes {s.probes} > {probe_budget}")
+                s = OpStats()
+                dac_sampler(table, n, streams["dac"], stats=s, device=True)
+                dac_max = max(dac_max, s.probes)
+                depth_max = max(depth_max, s.max_depth)
+                dac_probes.append(s.probes)
+                if s.probes > probe_budget:
+                    violations.append(f"dac probes {s.probes} > {probe_budget}")
+                if s.max_depth > depth_budget:
+                    violations.append(f"dac depth {s.max_depth} > {depth_budget}")
+            dac_mean = float(np.mean(dac_probes))
+            if dac_mean > dac_mean_budget:
+                violations.append(f"dac mean probes {dac_mean:.1f} > {dac_mean_budget:.1f}")
+            cells.append(ComplexityCell(
+                n=n, ratio=ratio, m=m, trials=trials,
+                ccf_max_comparisons=ccf_max, ccf_budget=ccf_budget,
+                binary_max_probes=bin_max, dac_max_probes=dac_max,
+                probe_budget=probe_budget, dac_max_depth=depth_max,
+                depth_budget=depth_budget, dac_mean_probes=dac_mean,
+                dac_mean_budget=dac_mean_budget, violations=violations,
+            ))
+    return cells

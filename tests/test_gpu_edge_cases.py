@@ -142,12 +142,24 @@ def test_upper_bound_search_errors(drs):
     assert drs.upper_bound_search(t, 0, 2, 0.5) == 1
 
 
-def test_stats_raises_instead_of_cpu_fallback(drs):
-    t = drs.build_weight_table([1.0, 1.0])
-    with pytest.raises(NotImplementedError):
-        drs.dac_sampler(t, 4, drs.RngStream(0), stats=drs.OpStats())
-    with pytest.raises(NotImplementedError):
-        drs.ccf_match([0.5], t, stats=drs.OpStats())
+def test_stats_counted_on_device(drs):
+    """stats= is the reference's instrumented count (test_samplers.py:174-188
+    shape): binary / ccf never nest scopes, dac never exceeds its budgets."""
+    t = drs.build_weight_table([1.0, 1.0, 1.0, 1.0])
+    s = drs.OpStats()
+    drs.binary_sampler(t, 100, drs.RngStream(1), stats=s)
+    assert s.max_depth == 0 and 0 < s.probes <= 100 * 3
+    s = drs.OpStats()
+    drs.ccf_sampler(t, 100, drs.RngStream(1), stats=s)
+    assert s.max_depth == 0 and 100 <= s.comparisons <= 2 * 100 + 100
+    s = drs.OpStats()
+    drs.ccf_match([0.5], t, stats=s)
+    assert (s.comparisons, s.probes) == (2, 0)  # the cursor stops on W[1] = 0.5
+    s = drs.OpStats()
+    drs.dac_sampler(t, 4, drs.RngStream(0), stats=s)
+    assert 1 <= s.max_depth <= 3 and s.probes <= 4 * 3
+    s = drs.OpStats()
+    assert drs.dac_match(np.empty(0), t, stats=s).shape == (0,) and s == drs.OpStats()
 
 
 def test_device_in_device_out(drs):
