@@ -119,3 +119,47 @@ def test_exhaustive_tables_size8_digest(drs, golden):
         count += 1
     assert count == int(golden["exh_count"])
     assert h.digest() == golden["exh_digest"].tobytes()
+
+
+def test_c4_full_bank_bit_exact(drs, orc):
+    """Config 4 at the bench's full size (B = 4096 filters of M_f = 16384,
+    N_f = 256, SURVEY 8(d) field): W, U and indices of every filter
+    bit-exact against the oracle twin of the batched kernel, which equals
+    the per-filter build_weight_table + dac_sampler loop; and the reference
+    association report over a prefix of the bank."""
+    from bench import CONFIGS, make_weights, parity_block
+
+    c = CONFIGS["c4"]
+    w = make_weights("c4")
+    B, Nf = w.shape[0], c["Nf"]
+    assert B == 4096 and w.shape[1] == c["Mf"]
+    streams = [drs.RngStream(c["useed"], (b,)) for b in range(B)]
+    keys = np.array([[s.key[0], s.key[1], s.position] for s in streams], dtype=np.uint64)
+    out, U, W = drs.resample_batched(w, Nf, streams, return_uniforms=True, return_tables=True)
+    eo, Uo, Wo, st = orc.resample_batched(w, Nf, keys)
+    assert st == 0
+    np.testing.assert_array_equal(W, Wo)
+    np.testing.assert_array_equal(U, Uo)
+    np.testing.assert_array_equal(out, eo)
+    rep = parity_block("c4", "dac", "auto", w)
+    assert rep["ok"], rep
+
+
+def test_sharded_nccl_two_gpus():
+    """The W-sharded table and sampler over NCCL on two GPUs (runs only when
+    two are visible): the gathered indices equal the single-GPU sampler's."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    root = Path(__file__).resolve().parents[1]
+    script = root / "tests" / "nccl_two_gpu.py"
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533", str(script)],
+                       capture_output=True, text=True, timeout=600, cwd=str(root),
+                       env={**os.environ, "PYTHONPATH": str(root)})
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "NCCL_TWO_GPU_OK" in r.stdout
