@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) k_op_counts(int kind, const double* __res
                                                    unsigned long long* counts) {
   unsigned long long probes = 0, depth = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < n; m += stride) {
+  for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; kind != 1 && m < n; m += stride) {
     if (kind == 2) {  // binary
       probes += bisect_probes(W, 0, M - 1, __ldg(u + m));
       continue;

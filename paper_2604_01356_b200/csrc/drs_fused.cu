@@ -697,6 +697,11 @@ extern "C" {
 int dr_debug_phase_times(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
 }
+int dr_debug_phase_clear(void) {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_phase) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(g_phase)) == cudaSuccess ? 0 : -1;
+}
 #endif
 
 int dr_sample_dac_from(const double* W, const double* idx, int64_t M, const double* raw, int64_t N,

@@ -18,8 +18,6 @@ namespace drs {
 
 IndexDesc make_index_desc(int64_t M);  // drs_scan.cu
 
-constexpr int TW = 4096;   // W entries per merge tile (32 KB)
-constexpr int UCH = 4096;  // u results staged per chunk (32 KB)
 constexpr int64_t DAC_TAU = 16;
 
 static int launch_rc() {
@@ -137,7 +135,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   const bool last = (j0 + len == M);
   const int len_even = len & ~1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  STAMPK(4, 0);
   pdl_wait();
+  STAMPK(4, 1);
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, (uint32_t)len_even * 8u);
@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   }
   __syncthreads();
   mbar_wait(&bar, 0);
+  STAMPK(4, 2);
   const int64_t ib = s_ib, ie = s_ie;
   // a long run: the whole MT_UC-chunks inside it are left to k_merge_heavy
   // (many CTAs), each marked in out[] by the first slot of the chunk holding
@@ -179,6 +180,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
       }
     }
     pdl_trigger();
+    STAMPK(4, 3);
     return;
   }
   for (int seg = 0; seg < 2; ++seg) {
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   // late (an early trigger: c2 45.0 us against 43.0): k_merge_heavy's CTAs
   // would take the slots of the last tiles
   pdl_trigger();
+  STAMPK(4, 3);
 }
 
 // The whole u-chunks of long runs (marked by k_merge_tiles): persistent CTAs
@@ -237,7 +240,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __rest
                                                             int64_t* __restrict__ out, int tw) {
   extern __shared__ __align__(128) double hsw[];  // [tw]
   __shared__ __align__(8) uint64_t bar;
+  STAMPK(5, 0);
   pdl_wait();
+  STAMPK(5, 1);
   pdl_trigger();
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
@@ -286,6 +291,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __rest
     }
     __syncthreads();  // s_mark reuse
   }
+  STAMPK(5, 3);
 }
 
 // -------------------------------------------------------------- checks ----
@@ -430,6 +436,17 @@ int launch_index(const double* W, const double* idx, int64_t M, const double* u,
 using namespace drs;
 
 extern "C" {
+
+#ifdef DRS_PHASE_TIMING
+int dr_debug_phase_times_match(unsigned long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
+}
+int dr_debug_phase_clear_match(void) {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_phase) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(g_phase)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int dr_validate_table(const double* W, int64_t M, int32_t* status, void* stream) {
   if (M < 1 || !W || !status) return DRS_ERR_ARG;

@@ -75,7 +75,9 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
                                                                int32_t* status_out, double* total_out,
                                                                int64_t chunk) {
   extern __shared__ __align__(16) double csm[];
+  STAMPK(1, 0);
   pdl_wait();
+  STAMPK(1, 1);
   STAMP1(0);
   pdl_trigger();  // one CTA: the next grid may take the other SMs now
   // [chunk + chunk / 32] tile totals -> exclusive in-group folds, one pad slot
@@ -182,11 +184,17 @@ __global__ void __launch_bounds__(CHAIN_THREADS) k_chain_groups(ScanWS ws, int64
   STAMP1(4);
   for (int64_t g = threadIdx.x; g < ng; g += CHAIN_THREADS) ws.grp[g] = sE[g];
   STAMP(5);
+  STAMPK(1, 3);
 }
 
 #ifdef DRS_PHASE_TIMING
 extern "C" int dr_debug_phase_times_scan(unsigned long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_phase, sizeof(unsigned long long) * (size_t)n) == cudaSuccess ? 0 : -1;
+}
+extern "C" int dr_debug_phase_clear_scan(void) {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_phase) != cudaSuccess) return -1;
+  return cudaMemset(p, 0, sizeof(g_phase)) == cudaSuccess ? 0 : -1;
 }
 #endif
 
@@ -422,7 +430,9 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
   __shared__ FoldSmem fs;
   __shared__ unsigned long long s_min;
   __shared__ uint64_t s_words[Src::SMEM_WORDS];
+  STAMPK(0, 0);
   pdl_wait();
+  STAMPK(0, 1);
   if (threadIdx.x == 0) s_min = 0x7FF0000000000000ULL;
   const int64_t t = blockIdx.x;
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
@@ -444,6 +454,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
     ws.agg[t] = A;
     ws.incl[t] = __longlong_as_double((long long)s_min);  // folded by k_chain_groups
   }
+  STAMPK(0, 2);
   pdl_trigger();
   double v[K_UNIF];
 #pragma unroll
@@ -455,6 +466,7 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
     for (int i = 0; i < K_UNIF; ++i)
       if (e0 + i < n) Z[e0 + i] = v[i];
   }
+  STAMPK(0, 3);
 }
 
 // pass 2: U = Z / Z[n] in place (memory-bound: 16 bytes per u), collapse
@@ -462,7 +474,9 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass1(Src src, int64_t n, Scan
 // the device stream advance follow in k_unif_finalize).
 __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, ScanWS ws, double* __restrict__ U) {
   __shared__ double s_last[WARPS];
+  STAMPK(2, 0);
   pdl_wait();
+  STAMPK(2, 1);
   constexpr int64_t TS = (int64_t)THREADS * K_UNIF;
   const int64_t t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -510,12 +524,15 @@ __global__ void __launch_bounds__(THREADS) k_unif_pass2(int64_t n, int64_t nt, S
       }
     }
   }
+  STAMPK(2, 3);
 }
 
 // after pass 2: the repair when pass 2 found collapse sites, the status word,
 // the device stream advance, counters back to zero
 __global__ void k_unif_finalize(ScanWS ws, int64_t n, double* U, int32_t* status_out, uint64_t* offset_dev) {
+  STAMPK(3, 0);
   pdl_wait();
+  STAMPK(3, 1);
   pdl_trigger();
   const uint32_t nsites = *(volatile uint32_t*)&ws.hdr->nsites;
   const uint32_t top = *(volatile uint32_t*)&ws.hdr->top;
@@ -528,6 +545,7 @@ __global__ void k_unif_finalize(ScanWS ws, int64_t n, double* U, int32_t* status
   if (offset_dev) *offset_dev += (uint64_t)(n + 1);  // every pass-1 CTA has read it
   ws.hdr->nsites = 0;
   ws.hdr->top = 0;
+  STAMPK(3, 3);
 }
 
 // ------------------------------------------------------------- uniforms ----
