@@ -370,6 +370,51 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
                        "algorithmic_bytes": 16 * M_, "launches": 3,
                        "note": "read w + write W (the index levels are extra); passes read w twice"}
 
+    # ---- the particle filter's resampling step (the paper's loop: new weights every
+    # step): build_weight_table + the benchmarked sampler, device-resident weights in
+    # and indices out, events; and end to end from pinned host weights to host indices
+    filter_step = None
+    if not light and cfg in ("c1", "c2", "c3"):
+        w_dev = torch.from_numpy(w_host).to(dev)
+        w_pin = torch.from_numpy(w_host).pin_memory()
+        fs_stream = drs.RngStream(c["useed"], (rank, 11))
+
+        def fstep_dev():
+            t_ = drs.build_weight_table(w_dev, check=False)
+            return sampler(t_, N, fs_stream, device=True, out=out_buf, **kw)
+
+        def fstep_e2e():
+            t_ = drs.build_weight_table(w_pin)  # pinned host weights: H2D inside, status read
+            return sampler(t_, N, fs_stream, **kw)  # host indices
+
+        for _ in range(2):
+            fstep_dev()
+            fstep_e2e()
+        torch.cuda.synchronize()
+        fs_ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            l2_flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fstep_dev()
+            b.record(s)
+            torch.cuda.synchronize()
+            fs_ms.append(a.elapsed_time(b))
+        reps = max(3, min(args.steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fstep_e2e()
+        torch.cuda.synchronize()
+        fe = (time.perf_counter() - t0) / reps
+        fsm = statistics.median(fs_ms)
+        fb = 16 * c["M"] + 16 * N  # table (read w, write W) + sampler (U + indices); W read by the search is extra
+        filter_step = {"ms": fsm, "samples_per_s": N / (fsm * 1e-3), "algorithmic_bytes": fb,
+                       "GB/s": fb / (fsm * 1e-3) / 1e9,
+                       "timed": "build_weight_table (device weights) + one sampler call, CUDA events, L2 flushed",
+                       "e2e": {"ms_per_step": 1e3 * fe, "h2d_bytes_per_step": 8 * c["M"], "d2h_bytes_per_step": 8 * N,
+                               "timer": "host perf_counter: pinned host weights -> table -> sampler -> host indices"}}
+        del w_dev, w_pin
+
     # ---- end to end through the public API, host result (and host weights for c4)
     e2e = None
     if e2e_step is not None:
@@ -423,6 +468,7 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps,
         "table_build": table_build,
+        "filter_step": filter_step,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
         "timing": "one public-API sampler call per step (device result), CUDA events on the launching stream",

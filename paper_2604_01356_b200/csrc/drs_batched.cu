@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
     sc1[w] = __dadd_rn(z0, z1);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mn = min(mn, (unsigned long long)__shfl_xor_sync(FULL, mn, o));
+  // rounded down to the high word (see block_min_u64): only the exactness trigger uses it
+  mn = (unsigned long long)__reduce_min_sync(FULL, (unsigned)(mn >> 32)) << 32;
   WSTAMP(3);
   __syncwarp();  // the words are consumed: the buffer holds the row totals now
   double* rows = buf;  // [w][33]: chunk totals of row w, then their bases Q (in place)
