@@ -173,6 +173,9 @@ class _Workspace:
 
 _ws: dict[tuple[int, int], _Workspace] = {}
 _ws_lock = threading.Lock()
+# superseded workspaces stay allocated: a CUDA graph captured earlier on the
+# stream may still point at them
+_ws_retired: list = []
 
 
 _ws_bytes: dict[tuple[int, int], int] = {}
@@ -200,6 +203,8 @@ def workspace(nbytes: int, st: int | None = None) -> tuple[int, int]:
         w = _ws.setdefault((dev, st), _Workspace())
         if w.nbytes < nbytes:
             size = max(nbytes, 2 * w.nbytes, 1 << 16)
+            if w.tensor is not None:
+                _ws_retired.append(w.tensor)
             w.tensor = torch.empty(size, dtype=torch.uint8, device=device())
             w.nbytes = size
             check(lib().dr_workspace_init(w.tensor.data_ptr(), size, st), "dr_workspace_init")
