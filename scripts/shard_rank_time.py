@@ -20,7 +20,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 import paper_2604_01356_b200 as drs  # noqa: E402
-from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable  # noqa: E402
+from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable, slice_capacity  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c5"
 c = bench.CONFIGS[cfg]
@@ -56,7 +56,8 @@ for G in (1, 2, 4, 8):
     tabs = []
     for g in range(G):
         W, idx = ops.finalize(scans[g][0], totals, G, g)
-        tabs.append(ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g, world=G))
+        tabs.append(ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g,
+                                       world=G, totals_host=totals.cpu().tolist()))
     del scans
     bounds = [nt * h // G for h in range(G + 1)]
     shares = [ops.unif_tile_totals((k0, k1), 0, N, bounds[h], bounds[h + 1]) for h in range(G)]
@@ -64,13 +65,17 @@ for G in (1, 2, 4, 8):
     zmin_all = torch.cat([z for _, z in shares])
     per = []
     for g in range(G):
+        ucap, ocap = slice_capacity(tabs[g], N, ts)
+        out = torch.empty(max(ocap, 1), dtype=torch.int64, device="cuda")
+
         def rank_step():
             ops.unif_tile_totals((k0, k1), 0, N, bounds[g], bounds[g + 1])
-            U, rng = ops.unif_local((k0, k1), 0, N, agg_all, zmin_all, totals, G, g)
-            ops.shard_match(tabs[g], U, rng)
-        U, rng = ops.unif_local((k0, k1), 0, N, agg_all, zmin_all, totals, G, g)
-        a, b, ta, tb = rng.tolist()
-        per.append({"rank": g, "ms": timed(rank_step), "draws": b - a, "tiles_regenerated": tb - ta + 1})
+            U, rng, _ = ops.unif_local((k0, k1), 0, N, agg_all, zmin_all, totals, G, g, ucap, ocap, False)
+            ops.shard_match(tabs[g], U, rng, N, out)
+        U, rng, st = ops.unif_local((k0, k1), 0, N, agg_all, zmin_all, totals, G, g, ucap, ocap, False)
+        a, b, ta, tb = rng.tolist()[:4]
+        per.append({"rank": g, "ms": timed(rank_step), "draws": b - a, "tiles_regenerated": tb - ta + 1,
+                    "status": int(st.item())})
     slowest = max(p["ms"] for p in per)
     res[f"G{G}"] = {"slowest_rank_ms": slowest, "sum_ms": sum(p["ms"] for p in per), "ranks": per}
     del tabs
