@@ -594,6 +594,43 @@ def cpu_baseline(cfg, sampler, seconds=10.0, threads=1):
             "ms_per_call": 1e3 * per}
 
 
+def reference_numba_baseline(cfg, seconds=3.0):
+    """The reference package itself (numba, single-threaded: SPEC.md:359) on this
+    host, when it is installed in baseline/_ref (pip install --no-deps --target
+    baseline/_ref of /root/reference/pkg): each sampler timed the reference's
+    way (bench.py:193-204: table built untimed, one call per timing, PCG64
+    streams) for about `seconds`; the C port in cpu_baseline is the pinned
+    restatement of the same code."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if cfg not in ("c1", "c2", "c3") or not (ref_dir / "dacresample").is_dir():
+        return {"unavailable": "config without a single table, or baseline/_ref not installed"}
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/drs_numba_cache")
+    sys.path.insert(0, str(ref_dir))
+    try:
+        import dacresample as ref
+        from dacresample.samplers import warm_kernels
+    except Exception as e:  # numba missing or the package broken: report, do not fail the bench
+        return {"unavailable": f"import failed: {e!r}"[:200]}
+    finally:
+        sys.path.remove(str(ref_dir))
+    c = CONFIGS[cfg]
+    table = ref.build_weight_table(make_weights(cfg))
+    warm_kernels()
+    out = {"kind": "reference", "cores": 1, "package": "baseline/_ref/dacresample (numba)"}
+    for name in ("dac", "ccf", "binary"):
+        fn = getattr(ref, f"{name}_sampler")
+        fn(table, c["N"], ref.RngStream(1))  # the read-only table specialisation compiles here
+        st = ref.RngStream(c["useed"])
+        calls, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            fn(table, c["N"], st)
+            calls += 1
+        per = (time.perf_counter() - t0) / calls
+        out[name] = {"ms_per_call": 1e3 * per, "value": (8 * c["M"] + 16 * c["N"]) / per / 1e9, "unit": "GB/s",
+                     "samples_per_s": c["N"] / per, "calls": calls}
+    return out
+
+
 def host_info():
     """CPU model and core counts of this host (the CPU baselines' hardware)."""
     model = None
@@ -720,6 +757,7 @@ def main():
                                      **{s: cpu_baseline(args.config, s, seconds=args.cpu_seconds / 2)
                                         for s in others}}
             line["cpu_host"] = host_info()
+            line["cpu_baselines"]["reference_numba"] = reference_numba_baseline(args.config)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
