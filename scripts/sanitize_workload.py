@@ -1,7 +1,10 @@
-"""A small workload that launches every libdrs kernel once or twice, for
-compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+"""A small workload that launches every libdrs kernel once or twice, meant
+for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
 
     compute-sanitizer --tool memcheck python scripts/sanitize_workload.py
+
+(compute-sanitizer is closed on the GPU pool this was built on, so it has run
+only without it; the parity tests are the bounds check there.)
 
 Sizes are small (the sanitizers slow kernels down 10-100x) but cross the
 tile, group and index-level edges: table builds (plain, log weights), the
