@@ -1,5 +1,5 @@
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import numpy as np, torch
 import paper_2604_01356_b200 as drs
 from paper_2604_01356_b200 import _lib, samplers
@@ -34,3 +34,8 @@ clock("dr_sample_dac ctypes (launch only)", lambda: L.dr_sample_dac(*args), 500)
 clock("dr_stream_synchronize after launch", lambda: (L.dr_sample_dac(*args), L.dr_stream_synchronize(s)), 500)
 clock("public dac_sampler device", lambda: drs.dac_sampler(table, N, st, device=True, out=o, uniforms_out=U), 500)
 clock("public dac_sampler host", lambda: drs.dac_sampler(table, N, st), 500)
+clock("public dac_sampler host, uniforms_out", lambda: drs.dac_sampler(table, N, st, uniforms_out=U), 500)
+clock("torch.cuda.current_device", torch.cuda.current_device)
+clock("_check_out(U)", lambda: samplers._check_out(U, N, torch.float64, "uniforms_out"))
+pin = host_result_i64(N)
+clock("launch + sync into one pinned buffer", lambda: (L.dr_sample_dac(W.data_ptr(), idx.data_ptr(), table.size, 1, 2, 0, 0, N, U.data_ptr(), pin.data_ptr(), sb.data_ptr(), 0, ws, wsb, s), L.dr_stream_synchronize(s)), 500)
