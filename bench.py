@@ -428,7 +428,8 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         e2e_step()
         torch.cuda.synchronize()
         one = time.perf_counter() - t0
-        e2e_calls = max(args.steps, min(2000, int(0.2 / max(one, 1e-6))))
+        # the same count on every rank: the sharded call holds a collective
+        e2e_calls = max(args.steps, min(2000, int(0.2 / max(one, 1e-6)))) if world == 1 else args.steps
         t0 = time.perf_counter()
         for _ in range(e2e_calls):
             e2e_step()
