@@ -1,4 +1,4 @@
-"""Worker of tests/test_gpu_c5.py::test_sharded_nccl_two_gpus (one rank per GPU, NCCL).
+"""Worker of tests/test_gpu_baseline_configs.py::test_sharded_nccl_two_gpus (one rank per GPU, NCCL).
 
 Builds a W-sharded table over the ranks, samples with both communication
 modes, gathers, and compares with the single-GPU dac_sampler on the whole

@@ -1,4 +1,4 @@
-"""Parity at BASELINE config 5 full size (M = 2^30, N = 2^24) and the
+"""Parity at every BASELINE config at full size -- config 5 (M = 2^30, N = 2^24), the
 north star's device-mode boundary report at every config.
 
 Config 5 is the box-scale case: an 8 GiB table with 8 index levels and byte
