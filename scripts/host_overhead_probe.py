@@ -39,3 +39,7 @@ clock("torch.cuda.current_device", torch.cuda.current_device)
 clock("_check_out(U)", lambda: samplers._check_out(U, N, torch.float64, "uniforms_out"))
 pin = host_result_i64(N)
 clock("launch + sync into one pinned buffer", lambda: (L.dr_sample_dac(W.data_ptr(), idx.data_ptr(), table.size, 1, 2, 0, 0, N, U.data_ptr(), pin.data_ptr(), sb.data_ptr(), 0, ws, wsb, s), L.dr_stream_synchronize(s)), 500)
+ob = torch.empty(N, dtype=torch.int64, device="cuda")
+clock("dr_sample_binary_dev ctypes (regular launch only)", lambda: L.dr_sample_binary_dev(W.data_ptr(), idx.data_ptr(), table.size, 1, 2, 0, 0, N, ob.data_ptr(), s), 500)
+clock("dr_match_binary ctypes (pdl launch only)", lambda: L.dr_match_binary(W.data_ptr(), idx.data_ptr(), table.size, U.data_ptr(), N, ob.data_ptr(), s), 500)
+clock("dr_version ctypes (no launch)", lambda: L.dr_version(), 2000)
