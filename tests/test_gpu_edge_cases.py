@@ -169,3 +169,49 @@ def test_device_in_device_out(drs):
     assert isinstance(out, torch.Tensor) and out.is_cuda and out.dtype == torch.int64
     out = drs.dac_sampler(t, 50, drs.RngStream(1), device=True)
     assert isinstance(out, torch.Tensor) and out.is_cuda
+
+
+def test_out_buffers_validated(drs):
+    """out= / uniforms_out= must be contiguous tensors of the right dtype and
+    length on the current device (or device-accessible pinned memory): a bad
+    buffer raises instead of being written out of bounds."""
+    t = drs.build_weight_table([1.0, 2.0, 3.0])
+    n = 64
+    with pytest.raises(ValueError, match="dtype"):
+        drs.dac_sampler(t, n, drs.RngStream(1), out=torch.empty(n, dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError, match="elements"):
+        drs.dac_sampler(t, n, drs.RngStream(1), out=torch.empty(n - 1, dtype=torch.int64, device="cuda"))
+    with pytest.raises(ValueError, match="contiguous"):
+        drs.ccf_sampler(t, n, drs.RngStream(1), out=torch.empty(2 * n, dtype=torch.int64, device="cuda")[::2])
+    with pytest.raises(ValueError, match="pinned"):
+        drs.binary_sampler(t, n, drs.RngStream(1), out=torch.empty(n, dtype=torch.int64))
+    with pytest.raises(ValueError, match="dtype"):
+        drs.dac_sampler(t, n, drs.RngStream(1), uniforms_out=torch.empty(n, dtype=torch.float32, device="cuda"))
+    with pytest.raises(TypeError):
+        drs.dac_sampler(t, n, drs.RngStream(1), out=np.empty(n, dtype=np.int64))
+    # pinned host buffers are written directly
+    out = torch.empty(n, dtype=torch.int64, pin_memory=True)
+    res = drs.dac_sampler(t, n, drs.RngStream(1), out=out, device=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out.numpy(), drs.dac_sampler(t, n, drs.RngStream(1)))
+    assert res.data_ptr() == out.data_ptr()
+
+
+def test_opstats_small_shapes(drs):
+    """Counts on the smallest shapes (values from the reference itself): one table entry (no probe ever), one u
+    (the root scope only), u = 1 exactly, and device-tensor inputs."""
+    one = drs.build_weight_table([5.0])
+    s = drs.OpStats()
+    drs.dac_match([0.3, 0.9, 1.0], one, stats=s)
+    assert (s.comparisons, s.probes) == (0, 0) and s.max_depth == 1  # the root scope is filled
+    t = drs.WeightTable([0.25, 0.5, 0.75, 1.0])
+    s = drs.OpStats()
+    drs.dac_match([0.6], t, stats=s)
+    assert (s.probes, s.max_depth) == (2, 1)
+    s = drs.OpStats()
+    drs.ccf_match(torch.tensor([0.1, 1.0], dtype=torch.float64, device="cuda"), t, stats=s)
+    assert s.comparisons == 3 + 2
+    s = drs.OpStats()
+    drs.binary_sampler(t, 3, __import__("tests.helpers", fromlist=["ReplayStream"]).ReplayStream([0.25, 0.5, 1.0]),
+                       stats=s)
+    assert s.probes == 6 and s.max_depth == 0
