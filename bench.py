@@ -415,6 +415,49 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
                                "timer": "host perf_counter: pinned host weights -> table -> sampler -> host indices"}}
         del w_dev, w_pin
 
+    # ---- the step after resampling: the resampled particle states,
+    # EnGMF layout (component = particle * N_Y + center, N_Y = M / N, d = 40):
+    # sampler + gather kernel (two calls) against resample_and_gather (the rows
+    # copied from the indices in registers in the single-kernel regime)
+    resample_gather = None
+    if not light and cfg in ("c1", "c2", "c3") and args.sampler == "dac":
+        ny, dd = c["M"] // N, 40
+        xs = torch.randn((N, dd), dtype=torch.float64, device=dev)
+        rg_stream = drs.RngStream(c["useed"], (rank, 12))
+
+        def rg_two():
+            i_ = drs.dac_sampler(table, N, rg_stream, device=True, out=out_buf)
+            return drs.gather_states(xs, i_, divisor=ny, check=False)  # no status read: no host sync
+
+        def rg_fused():
+            return drs.resample_and_gather(table, N, rg_stream, xs, divisor=ny)
+
+        def ev_median(fn, reps):
+            for _ in range(3):
+                fn()
+            ts = []
+            for _ in range(reps):
+                l2_flush()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                fn()
+                b.record(s)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            return statistics.median(ts)
+
+        reps = max(5, min(args.steps, 20))
+        t_two, t_fused = ev_median(rg_two, reps), ev_median(rg_fused, reps)
+        i_f, r_f = drs.resample_and_gather(table, N, drs.RngStream(c["useed"], (rank, 13)), xs, divisor=ny)
+        i_r = drs.dac_sampler(table, N, drs.RngStream(c["useed"], (rank, 13)), device=True)
+        same = bool(torch.equal(i_f, i_r) and torch.equal(r_f, xs[torch.div(i_r, ny, rounding_mode="floor")]))
+        rb = 2 * 8 * dd * N  # row reads + row writes
+        resample_gather = {"rows": N, "d": dd, "divisor": ny, "row_bytes": rb,
+                           "ms_sampler_then_gather": t_two, "ms_fused": t_fused,
+                           "speedup": t_two / t_fused, "identical": same,
+                           "timed": "CUDA events, L2 flushed, device table/states/result"}
+        del xs
+
     # ---- end to end through the public API, host result (and host weights for c4)
     e2e = None
     if e2e_step is not None:
@@ -478,6 +521,7 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         "gpu_launches": launches_per_step * args.steps,
         "table_build": table_build,
         "filter_step": filter_step,
+        "resample_gather": resample_gather,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
         "timing": "one public-API sampler call per step (device result), CUDA events on the launching stream",

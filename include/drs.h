@@ -142,6 +142,17 @@ int dr_sample_dac(const double *W, const double *idx, int64_t M, uint64_t k0, ui
                   uint64_t offset, uint64_t *offset_dev, int64_t N, double *U, int64_t *out,
                   int32_t *status, int32_t mode, void *ws, size_t ws_bytes, void *stream);
 
+/* dr_sample_dac followed by the step after resampling (the
+ * reference leaves it to the caller as states[idx]): gout[i][0..d) =
+ * states[out[i] / divisor][0..d), states row-major K x d fp64.  In the
+ * single-kernel regime the rows are copied from the indices still in
+ * registers (no re-read of out[]); otherwise a gather kernel follows the
+ * match on the stream.  DRS_ERR_ARG unless (M - 1) / divisor < K. */
+int dr_sample_dac_gather(const double *W, const double *idx, int64_t M, uint64_t k0, uint64_t k1,
+                         uint64_t offset, uint64_t *offset_dev, int64_t N, double *U, int64_t *out,
+                         const double *states, int64_t K, int64_t d, int64_t divisor, double *gout,
+                         int32_t *status, int32_t mode, void *ws, size_t ws_bytes, void *stream);
+
 /* dr_sample_dac with the N+1 underlying uniforms supplied (raw[N+1], a
  * duck-typed host stream such as the reference tests' ReplayStream). */
 int dr_sample_dac_from(const double *W, const double *idx, int64_t M, const double *raw, int64_t N,

@@ -26,7 +26,8 @@ from .samplers import (
     warm_kernels,
 )
 from .sharded import ShardedWeightTable, build_sharded_table, sharded_dac_sampler
-from .verify import chi_square_statistic, gather_states, histogram, verify_complexity, verify_statistics
+from .verify import (chi_square_statistic, gather_states, histogram, resample_and_gather, verify_complexity,
+                     verify_statistics)
 
 __all__ = [
     "RngStream",
@@ -51,6 +52,7 @@ __all__ = [
     "build_sharded_table",
     "sharded_dac_sampler",
     "gather_states",
+    "resample_and_gather",
     "histogram",
     "chi_square_statistic",
     "verify_statistics",

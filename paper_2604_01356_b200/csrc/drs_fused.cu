@@ -266,6 +266,12 @@ struct FusedArgs {
   int64_t* out;
   int32_t* status;
   ScanWS ws;
+  // optional: the step after resampling, fused with the index
+  // writes: gout[i][0..d) = states[out[i] / divisor][0..d), states[K][d] row-major
+  const double* states;
+  int64_t K, gd, divisor;
+  double* gout;  // null: no gather
+  bool gd_vec2;  // rows as 16-byte pairs (gd even, both bases aligned)
 };
 
 __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant__ FusedArgs a) {
@@ -491,6 +497,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
         if (e0 + i < n) a.U[e0 + i] = u[i];
     }
   }
+  if (a.gout) {
+    // the resampled particle states, straight from the indices in registers
+    // (lane l holds rows 2l, 2l+1 of the warp's 64).  The host checked
+    // (M - 1) / divisor < K, so every row exists.
+    const int64_t ew = t * TS_U + (int64_t)warp * LANES * K_UNIF;  // the warp's first draw
+    const int64_t rows = n - ew < LANES * K_UNIF ? n - ew : LANES * K_UNIF;
+    if (rows > 0) {
+      const int64_t s0 = r[0] / a.divisor, s1 = r[K_UNIF - 1] / a.divisor;
+      if (a.gd_vec2) gather_warp_rows<double2>((const double2*)a.states, a.gd / 2, s0, s1, rows,
+                                               (double2*)(a.gout + ew * a.gd), lane);
+      else gather_warp_rows<double>(a.states, a.gd, s0, s1, rows, a.gout + ew * a.gd, lane);
+    }
+  }
   __syncthreads();
   STAMP(8);
   if (t == 0 && threadIdx.x == 0) {
@@ -662,10 +681,20 @@ namespace drs {
 int sorted_uniforms_from_launch(const double* raw, int64_t n, double* U, int32_t* status, void* ws,
                                 size_t ws_bytes, cudaStream_t st);
 
+// the optional fused gather: gout[i] = states[out[i] / divisor] (K rows of gd)
+struct GatherSpec {
+  const double* states;
+  int64_t K, gd, divisor;
+  double* gout;
+};
+
+int launch_gather_rows(const double* states, int64_t K, int64_t d, const int64_t* idx, int64_t N, int64_t divisor,
+                       double* out, int32_t* status, cudaStream_t st);
+
 static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
                            uint64_t offset, uint64_t* offset_dev, const double* raw, int64_t N,
                            double* U, int64_t* out, int32_t* status, int32_t mode, void* ws,
-                           size_t ws_bytes, cudaStream_t st) {
+                           size_t ws_bytes, cudaStream_t st, const GatherSpec* g = nullptr) {
   if (M < 1 || N < 1 || !W || !out || !status || !ws || !U) return DRS_ERR_ARG;
   if (mode != DRS_DAC_AUTO && mode != DRS_DAC_MERGE && mode != DRS_DAC_SEARCH) return DRS_ERR_MODE;
   if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
@@ -679,6 +708,9 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
     a.k0 = k0; a.k1 = k1; a.offset = offset; a.offset_dev = offset_dev; a.raw = raw;
     a.n = N; a.U = U; a.out = out; a.status = status;
     a.ws = carve_ws(ws, ws_bytes);
+    a.states = g ? g->states : nullptr; a.gout = g ? g->gout : nullptr;
+    a.K = g ? g->K : 0; a.gd = g ? g->gd : 0; a.divisor = g ? g->divisor : 1;
+    a.gd_vec2 = g && (g->gd % 2 == 0) && ((((uintptr_t)g->states) | ((uintptr_t)g->gout)) & 15) == 0;
     void* args[] = {&a};
     const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3((unsigned)nt), dim3(THREADS),
                                                       args, (size_t)SIDX_CAP * 8, st);
@@ -687,7 +719,10 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
   const int rc = raw ? sorted_uniforms_from_launch(raw, N, U, status, ws, ws_bytes, st)
                      : sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
   if (rc) return rc;
-  return merge ? launch_merge(W, M, U, N, out, st) : launch_index(W, idx, M, U, N, out, st);
+  const int rm = merge ? launch_merge(W, M, U, N, out, st) : launch_index(W, idx, M, U, N, out, st);
+  if (rm || !g) return rm;
+  // two-pass pipeline: the gather follows the match on the stream
+  return launch_gather_rows(g->states, g->K, g->gd, out, N, g->divisor, g->gout, status, st);
 }
 }  // namespace drs
 
@@ -717,6 +752,18 @@ int dr_sample_dac(const double* W, const double* idx, int64_t M, uint64_t k0, ui
                   int32_t* status, int32_t mode, void* ws, size_t ws_bytes, void* stream) {
   return sample_dac_impl(W, idx, M, k0, k1, offset, offset_dev, nullptr, N, U, out, status, mode, ws,
                          ws_bytes, (cudaStream_t)stream);
+}
+
+int dr_sample_dac_gather(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
+                         uint64_t offset, uint64_t* offset_dev, int64_t N, double* U, int64_t* out,
+                         const double* states, int64_t K, int64_t d, int64_t divisor, double* gout,
+                         int32_t* status, int32_t mode, void* ws, size_t ws_bytes, void* stream) {
+  if (K < 1 || d < 1 || divisor < 1 || !states || !gout) return DRS_ERR_ARG;
+  // every index the sampler can return maps to a row: (M - 1) / divisor < K
+  if (M >= 1 && (M - 1) / divisor >= K) return DRS_ERR_ARG;
+  const GatherSpec g{states, K, d, divisor, gout};
+  return sample_dac_impl(W, idx, M, k0, k1, offset, offset_dev, nullptr, N, U, out, status, mode, ws,
+                         ws_bytes, (cudaStream_t)stream, &g);
 }
 
 int dr_sample_ccf(const double* W, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,

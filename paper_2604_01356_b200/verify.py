@@ -2,6 +2,9 @@
 
 * ``gather_states``: the step after resampling -- particle states by index
   (an EnGMF state row is d = 40 fp64, weightgen.py:37).
+* ``resample_and_gather``: ``dac_sampler`` and that gather in one library
+  call (``dr_sample_dac_gather``): in the single-kernel regime the rows are
+  copied from the indices still in registers.
 * ``histogram``: ``np.bincount(indices, minlength=m)`` (bench.py:241).
 * ``chi_square_statistic`` / ``verify_statistics``: the reference's Pearson
   goodness of fit (bench.py:221-246) with the counting and the statistic on
@@ -24,10 +27,11 @@ import torch
 from . import _lib
 from ._tensors import is_device_tensor, read_status, status_word, to_device_f64
 from .cdf import WeightTable, build_weight_table
-from .randkit import RngStream
+from .randkit import DeviceRngStream, RngStream
 from .samplers import OpStats, binary_sampler, ccf_sampler, dac_sampler
+from . import samplers as _samplers
 
-__all__ = ["gather_states", "histogram", "chi_square_statistic", "GofReport", "verify_statistics",
+__all__ = ["gather_states", "resample_and_gather", "histogram", "chi_square_statistic", "GofReport", "verify_statistics",
            "ComplexityCell", "verify_complexity", "dirichlet_uniform", "SAMPLER_ORDER"]
 
 SAMPLER_ORDER = ("dac", "ccf", "binary")  # bench.py:41
@@ -41,13 +45,15 @@ def _to_device_i64(x) -> tuple[torch.Tensor, bool]:
     return torch.from_numpy(a).to(_lib.device()), True
 
 
-def gather_states(states, indices, *, divisor: int = 1):
+def gather_states(states, indices, *, divisor: int = 1, check: bool = True):
     """Rows ``states[indices // divisor]`` (the resampled particles).
 
     ``states``: (K, d) float64 (numpy or CUDA tensor); ``indices``: int64[N]
     from a sampler.  ``divisor`` maps a mixture-component index to its
     particle (EnGMF: component = particle * N_Y + center, divisor = N_Y).
     Host inputs give a numpy (N, d) array, device inputs a CUDA tensor.
+    ``check=False`` skips the status read (no host synchronisation; rows of
+    out-of-range indices are then left unwritten).
     """
     s, host = to_device_f64(states)
     if s.ndim == 1:
@@ -61,9 +67,55 @@ def gather_states(states, indices, *, divisor: int = 1):
     st = status_word()
     _lib.check(_lib.lib().dr_gather_rows(s.data_ptr(), K, d, idx.data_ptr(), idx.numel(), int(divisor),
                                          out.data_ptr(), st.data_ptr(), _lib.stream_handle()), "dr_gather_rows")
-    if read_status(st) & _lib.ST_OUT_OF_SUPPORT:
+    if check and read_status(st) & _lib.ST_OUT_OF_SUPPORT:
         raise IndexError("index out of range for the states array")
     return out.cpu().numpy() if host else out
+
+
+def resample_and_gather(table: WeightTable, n: int, stream, states, *, divisor: int = 1, mode: str = "auto",
+                        device: bool = False):
+    """``idx = dac_sampler(table, n, stream)`` and ``gather_states(states, idx,
+    divisor=divisor)`` as one call; same draws, same indices, same rows.
+
+    ``stream``: RngStream or DeviceRngStream.  ``states``: (K, d) float64
+    with ``(table.size - 1) // divisor < K``.  Returns ``(indices, rows)``:
+    numpy for host states unless ``device``, else CUDA tensors.
+    """
+    if mode not in _lib.DAC_MODES:
+        raise ValueError(f"unknown mode {mode!r}")
+    if not isinstance(stream, (RngStream, DeviceRngStream)):
+        raise TypeError("resample_and_gather needs an RngStream or DeviceRngStream")
+    n, divisor = int(n), int(divisor)
+    if n < 0:
+        raise ValueError("n must be >= 0")
+    if divisor < 1:
+        raise ValueError("divisor must be >= 1")
+    s_, host = to_device_f64(states)
+    if s_.ndim == 1:
+        s_ = s_.reshape(-1, 1)
+    if s_.ndim != 2 or s_.shape[0] == 0:
+        raise ValueError("states must be (K, d) with K >= 1")
+    s_ = s_.contiguous()
+    K, d = int(s_.shape[0]), int(s_.shape[1])
+    if (table.size - 1) // divisor >= K:
+        raise IndexError("index out of range for the states array")
+    dev = _lib.device()
+    idx = torch.empty(n, dtype=torch.int64, device=dev)
+    rows = torch.empty((n, d), dtype=torch.float64, device=dev)
+    if n:
+        L = _lib.lib()
+        sh = _lib.stream_handle()
+        U = _samplers._scratch_uniforms(n, sh)
+        st = _samplers._status_buf(sh)
+        ws, wsb = _lib.workspace(_lib.workspace_bytes(_lib.OP_SORTED, n), sh)
+        k0, k1, off, offd = _samplers._stream_args(stream, n + 1)
+        _lib.check(L.dr_sample_dac_gather(table.device_cum.data_ptr(), _samplers._ptr(table.device_index),
+                                          table.size, k0, k1, off, offd, n, U.data_ptr(), idx.data_ptr(),
+                                          s_.data_ptr(), K, d, divisor, rows.data_ptr(), st.data_ptr(),
+                                          _lib.DAC_MODES[mode], ws, wsb, sh), "dr_sample_dac_gather")
+    if host and not device:
+        return idx.cpu().numpy(), rows.cpu().numpy()
+    return idx, rows
 
 
 def histogram(indices, m: int, *, device: bool = False):
