@@ -235,7 +235,7 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         e2e_h2d, e2e_d2h = 0, 8 * (N // world)
     else:
         w_host = make_weights(cfg)
-        table = drs.build_weight_table(w_host)
+        table = drs.build_weight_table(w_host, deferred=args.table == "deferred")
         M, N = c["M"], c["N"]
         stream = drs.RngStream(c["useed"], (rank,))
         alg_bytes = 8 * M + 16 * N
@@ -352,23 +352,31 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
     table_build = None
     if not light and (cfg in ("c1", "c2", "c3") or (cfg == "c5" and world == 1)):
         w_dev = torch.from_numpy(w_host).to(dev)
-        drs.build_weight_table(w_dev, check=False)
-        tb_ms = []
-        for _ in range(max(3, min(args.steps, 10))):
-            l2_flush()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(s)
-            drs.build_weight_table(w_dev, check=False)
-            b.record(s)
-            torch.cuda.synchronize()
-            tb_ms.append(a.elapsed_time(b))
+
+        def time_build(deferred):
+            drs.build_weight_table(w_dev, check=False, deferred=deferred)
+            ms = []
+            for _ in range(max(3, min(args.steps, 10))):
+                l2_flush()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                drs.build_weight_table(w_dev, check=False, deferred=deferred)
+                b.record(s)
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b))
+            return statistics.median(ms)
+
+        tbm = time_build(True)
+        tb2 = time_build(False)
         del w_dev
-        tbm = statistics.median(tb_ms)
         M_ = c["M"]
         table_build = {"ms": tbm, "GB/s": 16 * M_ / (tbm * 1e-3) / 1e9,
                        "frac": 16 * M_ / (tbm * 1e-3) / 1e9 / peak_hbm()[0],
-                       "algorithmic_bytes": 16 * M_, "launches": 3,
-                       "note": "read w + write W (the index levels are extra); passes read w twice"}
+                       "algorithmic_bytes": 16 * M_, "launches": 4,
+                       "note": "single pass (dr_build_table_deferred): read w once, write the table once, "
+                               "+ level 1 of the index read and written (M/16 each); local, chain, levels, guide",
+                       "two_pass_ms": tb2,
+                       "two_pass_note": "dr_build_table: pass 1 reads w, pass 2 reads w again and writes W"}
 
     # ---- the particle filter's resampling step (the paper's loop: new weights every
     # step): build_weight_table + the benchmarked sampler, device-resident weights in
@@ -509,6 +517,7 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         "data": "synthetic (seeded numpy weights, SURVEY.md 8(d)); Philox draws",
         "config": {
             "workload": cfg, **{k: v for k, v in c.items()}, "sampler": args.sampler, "mode": args.mode,
+            "table": args.table,
             "timed": "sorted uniforms + search per step, table resident (reference bench.py:193-204)",
             "l2": "flushed (256 MiB write) before every timed step; steps timed individually",
             "parallelism": ("shard-W" if cfg == "c5" else ("shard-filters" if cfg == "c4" else "replicas")) + f"x{world}",
@@ -728,6 +737,10 @@ def main():
     ap.add_argument("--sampler", default="dac", choices=["dac", "ccf", "binary"])
     ap.add_argument("--mode", default="auto", choices=["auto", "merge", "search"])
     ap.add_argument("--impl", default="drs", choices=["drs", "reference"])
+    ap.add_argument("--table", default="two-pass", choices=["deferred", "two-pass"],
+                    help="the sampled (resident) table: two-pass W (built once, sampled many times: the "
+                         "reference's timed region) or the single-pass deferred table (build_weight_table's "
+                         "default; the table_build and filter_step lines, where it is rebuilt every step)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--comm", default="allgather", choices=["allgather", "none"],

@@ -80,7 +80,20 @@ void dr_scan_geometry(int32_t g[6]);
 size_t dr_workspace_bytes(int op, int64_t M, int64_t N, int64_t B);
 int dr_workspace_init(void *ws, size_t ws_bytes, void *stream);
 
-/* doubles of the search index for an M-entry table (0 if M <= 16) */
+/* doubles of the index buffer `idx` of an M-entry table: the 16-ary search
+ * levels (none if M <= 16), the top guide, then the table header -- four
+ * doubles {T, deferred, 0, 0} -- and one {C_g, D_t} pair per table tile of
+ * DRS_SCAN_LANES * DRS_SCAN_WARPS * DRS_SCAN_K_TABLE entries.
+ *
+ * A table is a value array V[M] (the `W` argument of every search) plus idx.
+ * "Direct" tables (dr_build_table, dr_build_index) hold the cumulative
+ * weights in V.  "Deferred" tables (dr_build_table_deferred) hold the
+ * in-tile chained sums L of the single-pass build in V; their cumulative
+ * weights are W_j = fl((C_g + (D_t + L_j)) / T), bit-identical to
+ * dr_build_table's W, and every search compares C_g + (D_t + L_j) with the
+ * least s for which fl(s / T) >= u.  The searches read
+ * the header, so both kinds go through the same entry points; idx may be
+ * NULL only for a direct table with M <= 16. */
 int64_t dr_index_entries(int64_t M);
 
 /* build_weight_table (cdf.py:59-89): w[M] raw weights -> W[M] cumulative
@@ -89,6 +102,23 @@ int64_t dr_index_entries(int64_t M);
  * 16-byte aligned. */
 int dr_build_table(const double *w, int64_t M, double *W, double *idx, int32_t *status,
                    void *ws, size_t ws_bytes, void *stream);
+
+/* build_weight_table (cdf.py:59-89) in ONE pass over w (16 bytes per entry
+ * instead of 24): a deferred table (see dr_index_entries) with the same
+ * cumulative weights as dr_build_table; V[M] gets the in-tile sums, idx the
+ * index (levels hold W), the header and the tile pairs.  Status as
+ * dr_build_table.  w, V and idx must be 16-byte aligned. */
+int dr_build_table_deferred(const double *w, int64_t M, double *V, double *idx, int32_t *status,
+                            void *ws, size_t ws_bytes, void *stream);
+
+/* dr_build_table_log (below) as a deferred table: log-weights read once,
+ * the table written once, w never stored. */
+int dr_build_table_log_deferred(const double *logw, int64_t M, double *V, double *idx, int32_t *status,
+                                void *ws, size_t ws_bytes, void *stream);
+
+/* WeightTable.cum (cdf.py:20-30) of any table: W[j] = the cumulative weight
+ * (a copy of V for a direct table, formed for a deferred one). */
+int dr_table_materialize(const double *V, const double *idx, int64_t M, double *W, void *stream);
 
 /* The fused weight producer: the table of
  * w = exp(logw - max(logw)) -- weightgen.py:152-153 (engmf_weights' shift and
@@ -160,7 +190,7 @@ int dr_sample_dac_from(const double *W, const double *idx, int64_t M, const doub
                        size_t ws_bytes, void *stream);
 
 /* ccf_sampler (samplers.py:255-259): sorted uniforms then the streaming merge. */
-int dr_sample_ccf(const double *W, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,
+int dr_sample_ccf(const double *W, const double *idx, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,
                   uint64_t *offset_dev, int64_t N, double *U, int64_t *out, int32_t *status,
                   void *ws, size_t ws_bytes, void *stream);
 
@@ -172,7 +202,7 @@ int dr_sample_binary_dev(const double *W, const double *idx, int64_t M, uint64_t
 
 /* _ccf_kernel (samplers.py:100-107) for sorted U: W streamed once through
  * shared memory by TMA bulk copies, each tile merged with its U range. */
-int dr_match_ccf(const double *W, int64_t M, const double *U, int64_t N, int64_t *out,
+int dr_match_ccf(const double *W, const double *idx, int64_t M, const double *U, int64_t N, int64_t *out,
                  void *stream);
 
 /* _dac_kernel (samplers.py:110-146) for sorted U; mode DRS_DAC_*. */

@@ -237,6 +237,67 @@ int drs_ref_build_table(const double *w, int64_t M, double *W) {
   return st;
 }
 
+/* dr_build_table_deferred (the single-pass table): the same association as
+ * drs_ref_chain_scan, split at the tile prefix: V[j] = R + (Q + s) (the
+ * in-tile sums), per tile the pair {C_g, D_t}, so that S = C_g + (D_t + V[j]);
+ * idx = the index of W = min(S / T, 1), W[M-1] = 1 (drs_ref_build_table's W),
+ * then the header {T, 1, 0, 0} and the pairs.  W may be NULL. */
+int drs_ref_build_table_deferred(const double *w, int64_t M, double *V, double *idx, double *Wout) {
+  const int K = DRS_REF_K_TABLE;
+  const int64_t TS = DRS_REF_TABLE_TILE;
+  const int64_t nt = (M + TS - 1) / TS;
+  int st = 0;
+  for (int64_t j = 0; j < M; ++j)
+    if (!(w[j] >= 0.0 && w[j] < INFINITY)) st |= DRS_REF_ST_INVALID_WEIGHT;
+  double *P = (double *)malloc(sizeof(double) * 2 * (size_t)nt);
+  double *W = (double *)malloc(sizeof(double) * (size_t)M);
+  double C = 0.0, D = 0.0;
+  for (int64_t t = 0; t < nt; ++t) {
+    if (t > 0 && t % DRS_REF_GROUP == 0) {
+      C = C + D;
+      D = 0.0;
+    }
+    P[2 * t] = C;
+    P[2 * t + 1] = D;
+    double R = 0.0;
+    for (int wp = 0; wp < DRS_REF_WARPS; ++wp) {
+      double Q = 0.0;
+      for (int l = 0; l < DRS_REF_LANES; ++l) {
+        const int64_t base = t * TS + (int64_t)(wp * DRS_REF_LANES + l) * K;
+        double s = 0.0;
+        for (int i = 0; i < K; ++i) {
+          const int64_t j = base + i;
+          const double xi = (j < M) ? w[j] : 0.0;
+          s = (i == 0) ? xi : s + xi;
+          if (j < M) V[j] = R + (Q + s);
+        }
+        Q = Q + s;
+      }
+      R = R + Q;
+    }
+    D = D + R;
+  }
+  const double T = C + D;
+  if (T == 0.0) st |= DRS_REF_ST_DEGENERATE;
+  if (!(T < INFINITY)) st |= DRS_REF_ST_ACCUM_OVERFLOW;
+  for (int64_t j = 0; j < M; ++j) {
+    const int64_t t = j / TS;
+    W[j] = fmin((P[2 * t] + (P[2 * t + 1] + V[j])) / T, 1.0);
+  }
+  W[M - 1] = 1.0;
+  drs_ref_build_index(W, M, idx);
+  double *aux = idx + drs_ref_search_entries(M);
+  aux[0] = T;
+  aux[1] = 1.0;
+  aux[2] = 0.0;
+  aux[3] = 0.0;
+  memcpy(aux + 4, P, sizeof(double) * 2 * (size_t)nt);
+  if (Wout) memcpy(Wout, W, sizeof(double) * (size_t)M);
+  free(P);
+  free(W);
+  return st;
+}
+
 /* repair (randkit.py:104-116): forward nextafter chain, then backward. */
 void drs_port_repair_open_strict(double *u, int64_t n) {
   double lo = 0.0;
@@ -330,7 +391,8 @@ static void ref_top_guide(int64_t M, int *kt, int64_t *nkt, int *tshift, int64_t
   *tdoubles = ((n32 + 1) / 2 + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT * DRS_REF_FANOUT;
 }
 
-int64_t drs_ref_index_entries(int64_t M) {
+/* levels + top guide: the part of the index the searches descend */
+int64_t drs_ref_search_entries(int64_t M) {
   int64_t total = 0, n = M;
   while (n > DRS_REF_FANOUT) {
     n = (n + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT;
@@ -342,7 +404,15 @@ int64_t drs_ref_index_entries(int64_t M) {
   return total + td;
 }
 
+/* then the table header {T, deferred, 0, 0} and one {C_g, D_t} pair per
+ * table tile (mirrors include/drs.h dr_index_entries) */
+int64_t drs_ref_index_entries(int64_t M) {
+  return drs_ref_search_entries(M) + 4 + 2 * ((M + DRS_REF_TABLE_TILE - 1) / DRS_REF_TABLE_TILE);
+}
+
 void drs_ref_build_index(const double *W, int64_t M, double *idx) {
+  /* a direct table: header and tile pairs zero */
+  for (int64_t e = drs_ref_search_entries(M); e < drs_ref_index_entries(M); ++e) idx[e] = 0.0;
   int64_t n = M, off = 0;
   int64_t span = 1;
   while (n > DRS_REF_FANOUT) {

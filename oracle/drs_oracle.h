@@ -40,6 +40,7 @@ extern "C" {
 #define DRS_REF_K_UNIF 2
 #define DRS_REF_FANOUT 16
 #define DRS_REF_GROUP 32 /* tiles per group of the tile chain */
+#define DRS_REF_TABLE_TILE ((int64_t)DRS_REF_WARPS * DRS_REF_LANES * DRS_REF_K_TABLE)
 
 /* status bits (same values as include/drs.h) */
 #define DRS_REF_ST_INVALID_WEIGHT 0x1
@@ -65,6 +66,8 @@ int drs_ref_sorted_from_z(const double *z, int64_t n, double *U);
 int drs_ref_sorted_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, double *U);
 int drs_ref_sorted_uniforms_from(const double *raw, int64_t n, double *U);
 int64_t drs_ref_index_entries(int64_t M);
+int64_t drs_ref_search_entries(int64_t M);
+int drs_ref_build_table_deferred(const double *w, int64_t M, double *V, double *idx, double *Wout);
 void drs_ref_build_index(const double *W, int64_t M, double *idx);
 int drs_ref_build_table_sharded(const double *w, int64_t M, int G, double *W,
                                 double *shard_totals);

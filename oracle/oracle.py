@@ -36,6 +36,8 @@ _PROTOS = {
     "drs_ref_sorted_uniforms": (_INT, [_U64, _U64, _U64, _I64, _P]),
     "drs_ref_sorted_uniforms_from": (_INT, [_P, _I64, _P]),
     "drs_ref_index_entries": (_I64, [_I64]),
+    "drs_ref_search_entries": (_I64, [_I64]),
+    "drs_ref_build_table_deferred": (_INT, [_P, _I64, _P, _P, _P]),
     "drs_ref_build_index": (None, [_P, _I64, _P]),
     "drs_ref_build_table_sharded": (_INT, [_P, _I64, _INT, _P, _P]),
     "drs_ref_resample_batched": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
@@ -179,6 +181,22 @@ def build_index(W):
     out = np.empty(int(lib().drs_ref_index_entries(W.size)), dtype=np.float64)
     lib().drs_ref_build_index(_p(W), W.size, _p(out))
     return out
+
+
+def search_entries(M):
+    """doubles of the index the searches descend (levels + top guide)"""
+    return int(lib().drs_ref_search_entries(int(M)))
+
+
+def build_table_deferred(w):
+    """dr_build_table_deferred's outputs: (V in-tile sums, full idx with the
+    header and tile pairs, W, status)."""
+    w = _f64(w)
+    V = np.empty(w.size, dtype=np.float64)
+    W = np.empty(w.size, dtype=np.float64)
+    idx = np.empty(int(lib().drs_ref_index_entries(w.size)), dtype=np.float64)
+    st = lib().drs_ref_build_table_deferred(_p(w), w.size, _p(V), _p(idx), _p(W))
+    return V, idx, W, int(st)
 
 
 def match(kind, W, u):

@@ -55,6 +55,10 @@ _PROTOS = {
     "dr_index_entries": (_i64, [_i64]),
     "dr_build_table": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "dr_build_table_log": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_build_table_deferred": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_build_table_log_deferred": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size,
+                                           _c_void_p]),
+    "dr_table_materialize": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_validate_table": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_build_index": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_uniforms": (_int, [_u64, _u64, _u64, _i64, _c_void_p, _c_void_p]),
@@ -65,9 +69,9 @@ _PROTOS = {
     "dr_sample_dac": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
     "dr_sample_dac_gather": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
     "dr_sample_dac_from": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
-    "dr_sample_ccf": (_int, [_c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "dr_sample_ccf": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "dr_sample_binary_dev": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p]),
-    "dr_match_ccf": (_int, [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]),
+    "dr_match_ccf": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_match_dac": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _i32, _c_void_p]),
     "dr_check_sorted_open": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_lower_bound_range": (_int, [_c_void_p, _i64, _i64, _dbl, _c_void_p, _c_void_p]),

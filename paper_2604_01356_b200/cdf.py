@@ -3,9 +3,14 @@
 Mirrors /root/reference/pkg/src/dacresample/cdf.py: ``WeightTable`` (:20-56),
 ``build_weight_table`` (:59-89) and ``upper_bound_search`` (:92-126), with the
 same names, argument meaning and error messages.  The table lives in HBM:
-``W`` (fp64[M], ``W[M-1] == 1`` exactly) plus its 16-ary search index, built
-by one call of ``dr_build_table``.  ``.cum`` is a lazily mirrored, read-only
-host copy kept for reference compatibility.
+a value array (fp64[M]) plus its index buffer (16-ary search levels, top
+guide, table header).  ``build_weight_table`` makes a *deferred* table in one
+pass over the weights (``dr_build_table_deferred``): the values are the
+in-tile chained sums and the cumulative weights W_j = fl(S_j / T) are formed
+where a search compares them (include/drs.h); they are
+bit-identical to the two-pass ``dr_build_table``'s W.  ``WeightTable(cum)``
+makes a *direct* table holding ``cum`` itself.  ``.cum`` is a lazily mirrored,
+read-only host copy kept for reference compatibility.
 """
 
 from __future__ import annotations
@@ -39,10 +44,8 @@ def _raise_table_status(st: int) -> None:
         raise ValueError("cumulative weights must end at exactly 1")
 
 
-def _new_index(m: int) -> torch.Tensor | None:
-    n = int(_lib.lib().dr_index_entries(m))
-    if n == 0:
-        return None
+def _new_index(m: int) -> torch.Tensor:
+    n = int(_lib.lib().dr_index_entries(m))  # levels, top guide, table header: > 0 for every m
     return torch.empty(n, dtype=torch.float64, device=_lib.device())
 
 
@@ -58,13 +61,15 @@ class WeightTable:
     searches are reentrant.
     """
 
-    __slots__ = ("_W", "_idx", "_host")
+    __slots__ = ("_W", "_idx", "_host", "_deferred", "_cumdev")
 
     def __init__(self, cum, *, _built=None):
+        self._host = None
+        self._cumdev = None
         if _built is not None:
-            self._W, self._idx = _built
-            self._host = None
+            self._W, self._idx, self._deferred = _built
             return
+        self._deferred = False
         if is_device_tensor(cum):
             if cum.ndim != 1 or cum.numel() == 0:
                 raise ValueError("empty distribution")
@@ -83,14 +88,14 @@ class WeightTable:
         _raise_table_status(read_status(st))
         idx = _new_index(W.numel())
         _lib.check(L.dr_build_index(W.data_ptr(), W.numel(), _ptr(idx), s), "dr_build_index")
-        self._W, self._idx, self._host = W, idx, None
+        self._W, self._idx = W, idx
 
     # -- reference surface -------------------------------------------------
     @property
     def cum(self) -> np.ndarray:
         """Read-only host mirror of W (copied from the device on first use)."""
         if self._host is None:
-            h = self._W.cpu().numpy()
+            h = self.device_cum.cpu().numpy()
             h.flags.writeable = False
             self._host = h
         return self._host
@@ -104,7 +109,7 @@ class WeightTable:
 
     def weights(self) -> np.ndarray:
         """Per-index probabilities recovered from the cumulative sums (cdf.py:51-53)."""
-        W = self._W
+        W = self.device_cum
         return torch.diff(W, prepend=W.new_zeros(1)).cpu().numpy()
 
     def __repr__(self):
@@ -113,23 +118,43 @@ class WeightTable:
     # -- device surface ------------------------------------------------------
     @property
     def device_cum(self) -> torch.Tensor:
-        """W on the device (treat as read-only)."""
+        """W on the device (treat as read-only); a deferred table's is formed
+        once (``dr_table_materialize``) and kept."""
+        if not self._deferred:
+            return self._W
+        if self._cumdev is None:
+            W = torch.empty_like(self._W)
+            _lib.check(_lib.lib().dr_table_materialize(self._W.data_ptr(), self._idx.data_ptr(), self.size,
+                                                       W.data_ptr(), _lib.stream_handle()), "dr_table_materialize")
+            self._cumdev = W
+        return self._cumdev
+
+    @property
+    def device_values(self) -> torch.Tensor:
+        """The value array the searches read (W, or a deferred table's in-tile sums)."""
         return self._W
+
+    @property
+    def deferred(self) -> bool:
+        return self._deferred
 
     @property
     def device_index(self) -> torch.Tensor | None:
         return self._idx
 
 
-def build_weight_table(raw_weights, *, check: bool = True) -> WeightTable:
+def build_weight_table(raw_weights, *, check: bool = True, deferred: bool = True) -> WeightTable:
     """Normalize nonnegative weights into a :class:`WeightTable` (cdf.py:59-89).
 
-    One fused device pass pair: validate + chained fp64 scan + divide by the
-    total + pin ``W[M-1] = 1``, plus the search index.  Raises ``ValueError``
-    with the reference's messages ("empty distribution", "invalid weight",
-    "degenerate distribution", "accumulation overflow").  ``check=False``
-    skips the 4-byte status read (and therefore the host synchronisation)
-    for callers that validate elsewhere.
+    One pass over the weights (``deferred=True``, ``dr_build_table_deferred``):
+    validate + chained fp64 scan into in-tile sums, the tile chain, then the
+    index levels of W = S / T (``W[M-1] = 1``).  ``deferred=False`` runs the
+    two-pass build that stores W itself (``dr_build_table``); both tables have
+    the same W and give the same indices.  Raises ``ValueError`` with the
+    reference's messages ("empty distribution", "invalid weight", "degenerate
+    distribution", "accumulation overflow").  ``check=False`` skips the 4-byte
+    status read (and therefore the host synchronisation) for callers that
+    validate elsewhere.
     """
     if is_device_tensor(raw_weights):
         if raw_weights.ndim != 1 or raw_weights.numel() == 0:
@@ -149,23 +174,23 @@ def build_weight_table(raw_weights, *, check: bool = True) -> WeightTable:
     idx = _new_index(m)
     st = status_word()
     ws, wsb = _lib.workspace(L.dr_workspace_bytes(_lib.OP_TABLE, m, 0, 0))
-    _lib.check(
-        L.dr_build_table(w.data_ptr(), m, W.data_ptr(), _ptr(idx), st.data_ptr(), ws, wsb, _lib.stream_handle()),
-        "dr_build_table",
-    )
+    fn = "dr_build_table_deferred" if deferred else "dr_build_table"
+    _lib.check(getattr(L, fn)(w.data_ptr(), m, W.data_ptr(), idx.data_ptr(), st.data_ptr(), ws, wsb,
+                              _lib.stream_handle()), fn)
     if check:
         _raise_build_status(read_status(st))
-    return WeightTable(None, _built=(W, idx))
+    return WeightTable(None, _built=(W, idx, deferred))
 
 
-def build_weight_table_from_log(log_weights, *, check: bool = True) -> WeightTable:
+def build_weight_table_from_log(log_weights, *, check: bool = True, deferred: bool = True) -> WeightTable:
     """The table of ``exp(log_weights - log_weights.max())`` in one device pipeline.
 
     The fused weight producer of SURVEY 8(f): the reference's EnGMF field
     shifts its log-weights by the maximum and exponentiates
     (weightgen.py:152-153) before ``build_weight_table`` (cdf.py:59-89); here
-    a max reduction and the two table passes form the weights in shared
-    memory (device exp, within 1 ulp of np.exp), so w is never written.
+    a max reduction and one table pass (``deferred=False``: two) form the
+    weights in shared memory (device exp, within 1 ulp of np.exp), so w is
+    never written.
     Errors as ``build_weight_table`` (a NaN log-weight is an "invalid weight").
     """
     if is_device_tensor(log_weights):
@@ -186,13 +211,12 @@ def build_weight_table_from_log(log_weights, *, check: bool = True) -> WeightTab
     idx = _new_index(m)
     st = status_word()
     ws, wsb = _lib.workspace(L.dr_workspace_bytes(_lib.OP_TABLE, m, 0, 0))
-    _lib.check(
-        L.dr_build_table_log(lw.data_ptr(), m, W.data_ptr(), _ptr(idx), st.data_ptr(), ws, wsb, _lib.stream_handle()),
-        "dr_build_table_log",
-    )
+    fn = "dr_build_table_log_deferred" if deferred else "dr_build_table_log"
+    _lib.check(getattr(L, fn)(lw.data_ptr(), m, W.data_ptr(), idx.data_ptr(), st.data_ptr(), ws, wsb,
+                              _lib.stream_handle()), fn)
     if check:
         _raise_build_status(read_status(st))
-    return WeightTable(None, _built=(W, idx))
+    return WeightTable(None, _built=(W, idx, deferred))
 
 
 def upper_bound_search(table: WeightTable, lo: int, hi: int, x: float, stats=None) -> int:

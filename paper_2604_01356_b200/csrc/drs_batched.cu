@@ -74,25 +74,8 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase)
   }
 }
 
-// s*(x): the least double s with fl(s / T) >= x (division is monotone in s),
-// so that fl(S / T) < x <=> S < s*(x).  The candidates fl(x T) and its two
-// neighbours are divided together; a longer walk by ulps is rare.  T must be
-// positive and finite.
-__device__ __forceinline__ double s_star(double x, double T) {
-  const double sx = __dmul_rn(x, T);
-  const double sm = nextafter(sx, -dinf()), sp = nextafter(sx, dinf());
-  const double q0 = __ddiv_rn(sx, T), qm = __ddiv_rn(sm, T), qp = __ddiv_rn(sp, T);
-  if (q0 >= x) {
-    if (!(qm >= x)) return sx;
-    double r = sm;
-    for (double q = nextafter(sm, -dinf()); __ddiv_rn(q, T) >= x; q = nextafter(q, -dinf())) r = q;
-    return r;
-  }
-  if (qp >= x) return sp;
-  double r = sp;
-  do r = nextafter(r, dinf()); while (__ddiv_rn(r, T) < x);
-  return r;
-}
+// s*(x) = s_star (drs_common.cuh): the least double s with fl(s / T) >= x,
+// so that fl(S / T) < x <=> S < s*(x).
 
 // the exactness check and repair of randkit.py:95-116 on a filter's U (in
 // shared memory), by thread 0 and serially: rare, and N_f is small

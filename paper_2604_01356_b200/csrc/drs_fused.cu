@@ -32,7 +32,7 @@ ScanWS carve_ws(void* ws, size_t ws_bytes);
 int sorted_uniforms_launch(uint64_t k0, uint64_t k1, uint64_t offset, const uint64_t* offset_dev,
                            int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes,
                            cudaStream_t st);
-int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
+int launch_merge(const double* W, const double* idx, int64_t M, const double* U, int64_t N, int64_t* out,
                  cudaStream_t st);
 int launch_index(const double* W, const double* idx, int64_t M, const double* u, int64_t N,
                  int64_t* out, cudaStream_t st);
@@ -87,7 +87,7 @@ __device__ __forceinline__ int count_lt16_smem(const double* p, double x) {
 // lines of a level are in flight together
 __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const double* __restrict__ idx,
                                             const double* sidx, const IndexDesc& d, const SmemLevels& sl,
-                                            const double x[K_UNIF], int64_t r[K_UNIF]) {
+                                            const TabAux& ta, const double x[K_UNIF], int64_t r[K_UNIF]) {
   int64_t b[K_UNIF];
 #pragma unroll
   for (int q = 0; q < K_UNIF; ++q) b[q] = 0;
@@ -131,8 +131,10 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
     }
   }
   // W level: the lines are loaded together (branch-free addresses; the rare
-  // short tail line is re-read scalar), so the DRAM round trips overlap
+  // short tail line is re-read scalar), so the DRAM round trips overlap; a
+  // deferred table's tile pairs and keys are formed while they are in flight
   double v[K_UNIF][16];
+  double2 cd[K_UNIF];
 #pragma unroll
   for (int q = 0; q < K_UNIF; ++q) {
     const int64_t j0 = FANOUT * b[q];
@@ -141,18 +143,17 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
     ldg256(p + 4, v[q][4], v[q][5], v[q][6], v[q][7]);
     ldg256(p + 8, v[q][8], v[q][9], v[q][10], v[q][11]);
     ldg256(p + 12, v[q][12], v[q][13], v[q][14], v[q][15]);
+    cd[q] = ta.def ? __ldg(ta.P + j0 / TABLE_TILE) : make_double2(0.0, 0.0);
   }
+  WKey key[K_UNIF];
+#pragma unroll
+  for (int q = 0; q < K_UNIF; ++q) key[q] = tab_wkey(ta, x[q]);
 #pragma unroll
   for (int q = 0; q < K_UNIF; ++q) {
     const int64_t j0 = FANOUT * b[q];
     const int64_t valid = d.n[0] - j0;
-    int c = 0;
-    if (valid >= FANOUT) {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) c += (v[q][i] < x[q]) ? 1 : 0;
-    } else {
-      for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
-    }
+    int c = (valid >= FANOUT) ? count_w16(v[q], ta, cd[q], x[q], key[q])
+                              : count_w_tail(W, j0, (int)valid, ta, cd[q], x[q]);
     if (c >= valid) c = (int)valid - 1;
     r[q] = j0 + c;
   }
@@ -177,10 +178,30 @@ __device__ __forceinline__ int count_lt16_half(const double* p, double x) {
   return c;
 }
 
+// the same on a W line of a deferred table: S_j against the key (band test
+// of tab_wkey, the exact quotient inside the band)
+__device__ __forceinline__ bool w_below(const TabAux& ta, double S, double x, const WKey& k) {
+  if (S < k.lo) return true;
+  if (S > k.hi || !(S >= k.lo)) return false;  // above the band, or NaN key
+  return __ddiv_rn(S, ta.T) < x;
+}
+__device__ __forceinline__ int count_w16_half(const double* p, const TabAux& ta, double2 cd, double x, const WKey& k) {
+  if (!ta.def) return count_lt16_half(p, x);
+  const bool up = w_below(ta, tab_sum(ta, cd, __ldg(p + 7)), x, k);
+  const double* h = p + (up ? 8 : 0);
+  double v[8];
+  ldg256(h + 0, v[0], v[1], v[2], v[3]);
+  ldg256(h + 4, v[4], v[5], v[6], v[7]);
+  int c = up ? 8 : 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) c += w_below(ta, tab_sum(ta, cd, v[i]), x, k) ? 1 : 0;
+  return c;
+}
+
 template <int KQ>
 __device__ __forceinline__ void search_half(const double* __restrict__ W, const double* __restrict__ idx,
                                             const double* sidx, const IndexDesc& d, const SmemLevels& sl,
-                                            const double x[KQ], int64_t r[KQ]) {
+                                            const TabAux& ta, const double x[KQ], int64_t r[KQ]) {
   int64_t b[KQ];
 #pragma unroll
   for (int q = 0; q < KQ; ++q) b[q] = 0;
@@ -221,16 +242,19 @@ __device__ __forceinline__ void search_half(const double* __restrict__ W, const 
       b[q] = FANOUT * b[q] + c[q];
     }
   }
+  double2 cd[KQ];
+  WKey key[KQ];
+#pragma unroll
+  for (int q = 0; q < KQ; ++q) {
+    cd[q] = ta.def ? __ldg(ta.P + FANOUT * b[q] / TABLE_TILE) : make_double2(0.0, 0.0);
+    key[q] = tab_wkey(ta, x[q]);
+  }
 #pragma unroll
   for (int q = 0; q < KQ; ++q) {
     const int64_t j0 = FANOUT * b[q];
     const int64_t valid = d.n[0] - j0;
-    int c = 0;
-    if (valid >= FANOUT) {
-      c = count_lt16_half(W + j0, x[q]);
-    } else {
-      for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
-    }
+    int c = (valid >= FANOUT) ? count_w16_half(W + j0, ta, cd[q], x[q], key[q])
+                              : count_w_tail(W, j0, (int)valid, ta, cd[q], x[q]);
     if (c >= valid) c = (int)valid - 1;
     r[q] = j0 + c;
   }
@@ -313,8 +337,16 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
     const int64_t p0 = plo + t * per, p1 = min(a.sl.base, p0 + per) & ~(int64_t)1;
     for (int64_t p = p0 & ~(int64_t)1; p < p1; p += 8192)  // 64 KB pieces
       prefetch_l2(a.idx + p, (uint32_t)(min((int64_t)8192, p1 - p) * 8));
+    // the table's tile pairs (a deferred table's W line needs its tile's
+    // pair: 16 bytes per 8448 entries, 127 KB at M = 2^26), one slice per CTA
+    const int64_t pb = a.d.aoff + TAB_HDR, pn = 2 * table_tiles(a.d.n[0]);
+    const int64_t pper = cdiv(cdiv(pn, (int64_t)gridDim.x), 2) * 2;
+    const int64_t q0 = t * pper, q1 = min(pn, q0 + pper);
+    for (int64_t q = q0; a.idx && q < q1; q += 8192)
+      prefetch_l2(a.idx + pb + q, (uint32_t)(min((int64_t)8192, q1 - q) * 8));
   }
   const unsigned long long gen = *(volatile unsigned long long*)&a.ws.hdr->fgen;
+  const TabAux ta = load_aux(a.idx ? a.idx + a.d.aoff : nullptr);  // consumed by the search
   const uint64_t offset = a.offset_dev ? *(volatile uint64_t*)a.offset_dev : a.offset;
   __syncthreads();
   STAMP(0);
@@ -476,7 +508,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   mbar_wait(&bar, 0);
   STAMP(6);
   int64_t r[K_UNIF];
-  search_k_sm(a.W, a.idx, sidx, a.d, a.sl, u, r);
+  search_k_sm(a.W, a.idx, sidx, a.d, a.sl, ta, u, r);
   STAMP(7);
 
   // 6. write back: one 16-byte store per lane when aligned, so a warp's
@@ -558,6 +590,7 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t off = offset_dev ? *(volatile uint64_t*)offset_dev : offset;
+  const TabAux ta = load_aux(idx ? idx + d.aoff : nullptr);
   bool staged = false;
   static_assert(K_UNIF == 2, "two draws per thread per chunk");
   for (int64_t base = (int64_t)blockIdx.x * 2 * blockDim.x; base < N; base += (int64_t)gridDim.x * 2 * blockDim.x) {
@@ -574,7 +607,7 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
       staged = true;
     }
     int64_t r[K_UNIF];
-    search_k_sm(W, idx, sidx, d, sl, u, r);
+    search_k_sm(W, idx, sidx, d, sl, ta, u, r);
 #pragma unroll
     for (int h = 0; h < K_UNIF; ++h)
       if (i[h] < N) out[i[h]] = r[h];
@@ -613,6 +646,7 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   __syncthreads();
   pdl_trigger();
   mbar_wait(&bar, 0);
+  const TabAux ta = load_aux(idx ? idx + d.aoff : nullptr);
   const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
   if (rng) {  // sharded: U and out are windows with global bases rng[4], rng[5]
     u -= rng[4];
@@ -629,8 +663,8 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
       x[h] = (i[h] < hi) ? __ldg(u + i[h]) : 0.5;
     }
     int64_t r[KQ];
-    if constexpr (THROUGHPUT) search_half<KQ>(W, idx, sidx, d, sl, x, r);
-    else search_k_sm(W, idx, sidx, d, sl, x, r);
+    if constexpr (THROUGHPUT) search_half<KQ>(W, idx, sidx, d, sl, ta, x, r);
+    else search_k_sm(W, idx, sidx, d, sl, ta, x, r);
 #pragma unroll
     for (int h = 0; h < KQ; ++h)
       if (i[h] < hi) out[i[h]] = shift + r[h];
@@ -719,7 +753,7 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
   const int rc = raw ? sorted_uniforms_from_launch(raw, N, U, status, ws, ws_bytes, st)
                      : sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
   if (rc) return rc;
-  const int rm = merge ? launch_merge(W, M, U, N, out, st) : launch_index(W, idx, M, U, N, out, st);
+  const int rm = merge ? launch_merge(W, idx, M, U, N, out, st) : launch_index(W, idx, M, U, N, out, st);
   if (rm || !g) return rm;
   // two-pass pipeline: the gather follows the match on the stream
   return launch_gather_rows(g->states, g->K, g->gd, out, N, g->divisor, g->gout, status, st);
@@ -766,7 +800,7 @@ int dr_sample_dac_gather(const double* W, const double* idx, int64_t M, uint64_t
                          ws_bytes, (cudaStream_t)stream, &g);
 }
 
-int dr_sample_ccf(const double* W, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,
+int dr_sample_ccf(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1, uint64_t offset,
                   uint64_t* offset_dev, int64_t N, double* U, int64_t* out, int32_t* status, void* ws,
                   size_t ws_bytes, void* stream) {
   if (M < 1 || N < 1 || !W || !U || !out || !status || !ws) return DRS_ERR_ARG;
@@ -774,7 +808,7 @@ int dr_sample_ccf(const double* W, int64_t M, uint64_t k0, uint64_t k1, uint64_t
   cudaStream_t st = (cudaStream_t)stream;
   int rc = sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
   if (rc) return rc;
-  return launch_merge(W, M, U, N, out, st);
+  return launch_merge(W, idx, M, U, N, out, st);
 }
 
 int dr_sample_binary_dev(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,

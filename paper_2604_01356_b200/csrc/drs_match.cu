@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(256) k_match_index(const double* __restrict__ 
                                                      int64_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= N) return;
-  out[i] = index_lower_bound(W, idx, d, __ldg(u + i));
+  out[i] = index_lower_bound(W, idx, d, load_aux(idx ? idx + d.aoff : nullptr), __ldg(u + i));
 }
 
 // fused binary_sampler: the warp's 32 consecutive draws come from <= 9 Philox
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) k_sample_binary(const double* __restrict_
   const int wi = (int)(dd & 3);
   const uint64_t raw = wi == 0 ? w0 : (wi == 1 ? w1 : (wi == 2 ? w2 : w3));
   const int64_t i = base + lane;
-  if (i < N) out[i] = index_lower_bound(W, idx, d, u01(raw));
+  if (i < N) out[i] = index_lower_bound(W, idx, d, load_aux(idx ? idx + d.aoff : nullptr), u01(raw));
 }
 
 // -------------------------------------------------------- K5 merge stream ----
@@ -114,12 +114,37 @@ __device__ __forceinline__ int smem_lower_bound(const double* a, int n, double x
   return lo;
 }
 
+// a staged W tile sw[0..len) of entries j0.. of a deferred table -> W itself:
+// S = C_g + (D_t + L), W = min(S / T, 1) (the division by the shared T as a
+// multiply and two FMAs, div_rn), W[M-1] = 1.  The pair is re-read per entry
+// from L1 (holding both in registers costs k_merge_tiles its eighth CTA per SM).
+__device__ __forceinline__ void stage_to_w(double* sw, int len, int64_t j0, int64_t M, const TabAux& ta) {
+  const double2* P = ta.P + j0 / TABLE_TILE;
+  const int jb = (int)((j0 / TABLE_TILE + 1) * TABLE_TILE - j0);
+  const int il = (M - 1 - j0 < (int64_t)len) ? (int)(M - 1 - j0) : -1;  // the pinned last entry, if in this tile
+  const DivBy byT = div_by(ta.T);
+  for (int i = threadIdx.x; i < len; i += blockDim.x) {
+    const double2 cd = __ldg(P + (i < jb ? 0 : 1));
+    sw[i] = (i == il) ? 1.0 : fmin(div_rn(__dadd_rn(cd.x, __dadd_rn(cd.y, sw[i])), byT), 1.0);
+  }
+}
+
+// W[j] at the end of a 16-entry block (j = 16 m + 15, or M - 1): level 1 of
+// the index holds exactly these values for either kind of table (W itself,
+// never a deferred table's in-tile value); a table without an index is direct
+__device__ __forceinline__ double block_end_w(const double* __restrict__ W, const double* __restrict__ idx,
+                                              int64_t M, int64_t j) {
+  return (idx && M > FANOUT) ? __ldg(idx + j / FANOUT) : __ldg(W + j);  // level 1 sits at offset 0
+}
+
 constexpr int MT_THREADS = 256;
 constexpr int MT_TW = 4096;   // max W entries per tile (32 KB)
 constexpr int MT_UC = 1024;   // u's staged per merge-path chunk (8 KB)
 constexpr int MT_HEAVY = 4 * MT_UC;  // a tile's u-run longer than this is spread over k_merge_heavy
 
-__global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __restrict__ W, int64_t M,
+__global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __restrict__ W, int64_t M,
+                                                            const double* __restrict__ idx,
+                                                            const double* __restrict__ aux,
                                                             const double* __restrict__ U, int64_t N,
                                                             int64_t* __restrict__ out, int tw, int paths) {
   extern __shared__ __align__(128) double msm[];
@@ -129,6 +154,9 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   __shared__ __align__(8) uint64_t bar;
   __shared__ int64_t s_ib, s_ie;
   __shared__ int s_w0, s_w1;
+  __shared__ double2 s_hdr;  // the table header {T, deferred}, read beside the u-run searches
+  __shared__ double2 s_pair[2];  // a deferred table's tile pairs around j0
+  __shared__ int s_probe;        // deferred, few u's: W formed at each bisection probe
   const int64_t t = blockIdx.x;
   const int64_t j0 = t * tw;
   const int len = (int)((M - j0) < tw ? (M - j0) : tw);
@@ -144,17 +172,32 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
     if (len_even > 0) bulk_g2s(sw, W + j0, (uint32_t)len_even * 8u, &bar);
   }
   if (threadIdx.x == 64 && (len & 1)) sw[len - 1] = W[j0 + len - 1];
-  if (warp == 0) {
-    const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, __ldg(W + j0 - 1));
+  if (threadIdx.x >= 96 && threadIdx.x < 99) {
+    // the table header and a deferred table's tile pairs around j0 (unused,
+    // all zero, for a direct table), loaded beside the u-run searches
+    if (threadIdx.x == 96) s_hdr = aux ? __ldg(reinterpret_cast<const double2*>(aux)) : make_double2(1.0, 0.0);
+    else if (aux) s_pair[threadIdx.x - 97] = __ldg(reinterpret_cast<const double2*>(aux + TAB_HDR) +
+                                                   min(j0 / TABLE_TILE + (threadIdx.x - 97), table_tiles(M) - 1));
+    s_probe = 0;
+  }
+  if (warp == 0) {  // tile edges are block ends (tw is a multiple of 16): level 1 holds W there
+    const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, block_end_w(W, idx, M, j0 - 1));
     if (lane == 0) s_ib = v;
   } else if (warp == 1) {
-    const int64_t v = last ? N : warp_count_le(U, N, __ldg(W + j0 + len - 1));
+    const int64_t v = last ? N : warp_count_le(U, N, block_end_w(W, idx, M, j0 + len - 1));
     if (lane == 0) s_ie = v;
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  STAMPK(4, 2);
   const int64_t ib = s_ib, ie = s_ie;
+  // a deferred table: a tile holding many u's becomes W once (a multiply and
+  // two FMAs per entry); one holding few (M >> N) forms W at each probe
+  if (s_hdr.y != 0.0) {
+    if (16 * (ie - ib) > (int64_t)len) stage_to_w(sw, len, j0, M, load_aux(aux));
+    else if (threadIdx.x == 0) s_probe = 1;
+    __syncthreads();
+  }
+  STAMPK(4, 2);
   // a long run: the whole MT_UC-chunks inside it are left to k_merge_heavy
   // (many CTAs), each marked in out[] by the first slot of the chunk holding
   // -1 - t; this CTA keeps the ragged ends [ib, sk0) and [sk1, ie)
@@ -171,10 +214,22 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
       for (int64_t i = r0 + threadIdx.x; i < r1; i += MT_THREADS) {
         const double x = __ldg(U + i);
         int lo = 0, hi = len - 1;
-        while (lo < hi) {
-          const int mid = (lo + hi) >> 1;
-          if (sw[mid] < x) lo = mid + 1;
-          else hi = mid;
+        if (*(volatile int*)&s_probe) {
+          const int jb = (int)((j0 / TABLE_TILE + 1) * TABLE_TILE - j0);
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const double2 cd = s_pair[mid < jb ? 0 : 1];
+            const double v = (j0 + mid == M - 1)
+                                 ? 1.0 : fmin(__ddiv_rn(__dadd_rn(cd.x, __dadd_rn(cd.y, sw[mid])), s_hdr.x), 1.0);
+            if (v < x) lo = mid + 1;
+            else hi = mid;
+          }
+        } else {
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sw[mid] < x) lo = mid + 1;
+            else hi = mid;
+          }
         }
         out[i] = j0 + lo;
       }
@@ -187,7 +242,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
   const int64_t r0 = seg ? sk1 : ib, r1 = seg ? ie : sk0;
   for (int64_t c0 = r0; c0 < r1; c0 += MT_UC) {
     const int c = (int)((r1 - c0) < MT_UC ? (r1 - c0) : MT_UC);
-    for (int i = threadIdx.x; i < c; i += MT_THREADS) su[i] = __ldg(U + c0 + i);
+    for (int i = threadIdx.x; i < c; i += MT_THREADS) su[i] = __ldg(U + c0 + i);  // (a deferred tile is W here)
     __syncthreads();
     // the chunk's u's land in sw[wa0 .. wa1] (wa0 = lower bound of its first
     // u, wa1 of its last): merge only that part of the tile
@@ -236,6 +291,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_tiles(const double* __rest
 // stride over the chunks, skip unmarked ones (one load), stage the marked
 // chunk's W tile by TMA (kept while consecutive chunks share it) and bisect.
 __global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __restrict__ W, int64_t M,
+                                                            const double* __restrict__ aux,
                                                             const double* __restrict__ U, int64_t N,
                                                             int64_t* __restrict__ out, int tw) {
   extern __shared__ __align__(128) double hsw[];  // [tw]
@@ -246,6 +302,7 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __rest
   pdl_trigger();
   if (threadIdx.x == 0) mbar_init(&bar, 1);
   __syncthreads();
+  const TabAux ta = load_aux(aux);
   __shared__ int64_t s_mark[MT_THREADS];
   uint32_t phase = 0;
   int64_t cur = -1;
@@ -275,6 +332,10 @@ __global__ void __launch_bounds__(MT_THREADS) k_merge_heavy(const double* __rest
         mbar_wait(&bar, phase);
         phase ^= 1u;
         __syncthreads();
+        if (ta.def) {  // a heavy tile serves >= 1024 u's: W itself
+          stage_to_w(hsw, len, j0, M, ta);
+          __syncthreads();
+        }
         cur = t;
       }
       for (int64_t i = k * MT_UC + threadIdx.x; i < (k + 1) * MT_UC; i += MT_THREADS) {
@@ -352,8 +413,9 @@ __global__ void k_lower_bound_range(const double* __restrict__ W, int64_t lo, in
   out[1] = probes;
 }
 
-int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t* out,
+int launch_merge(const double* W, const double* idx, int64_t M, const double* U, int64_t N, int64_t* out,
                  cudaStream_t st) {
+  const double* aux = idx ? idx + make_index_desc(M).aoff : nullptr;
   static SmemLimit lim;
   lim.raise((const void*)k_merge_tiles, (MT_TW + 2 * MT_UC) * sizeof(double));
   const int sms = drs_sm_count();
@@ -366,14 +428,14 @@ int launch_merge(const double* W, int64_t M, const double* U, int64_t N, int64_t
   // flight per SM; a tile that still holds a long run bisects every u
   const int paths = (double)N * tw >= 64.0 * (double)M ? 1 : 0;
   const size_t smem = (size_t)(tw + (paths ? 2 * MT_UC : 0)) * sizeof(double);
-  launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, U, N, out, tw,
+  launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, idx, aux, U, N, out, tw,
              paths);
   if (N > MT_HEAVY) {  // a run can be long: the helper grid (it exits after one load per chunk otherwise)
     static SmemLimit hl;
     hl.raise((const void*)k_merge_heavy, (size_t)MT_TW * sizeof(double));
     const int64_t nch = N / MT_UC;
     const unsigned g = (unsigned)(nch < 2 * (int64_t)sms ? nch : 2 * (int64_t)sms);
-    launch_pdl(k_merge_heavy, dim3(g), dim3(MT_THREADS), (size_t)tw * sizeof(double), st, W, M, U, N, out, tw);
+    launch_pdl(k_merge_heavy, dim3(g), dim3(MT_THREADS), (size_t)tw * sizeof(double), st, W, M, aux, U, N, out, tw);
   }
   return launch_rc();
 }
@@ -410,8 +472,18 @@ int launch_top_guide(int64_t M, double* idx, cudaStream_t st) {
   return launch_rc();
 }
 
+// the header and tile pairs of a direct table, all zero (deferred = 0:
+// searches compare W itself)
+int write_direct_header(double* idx, int64_t M, cudaStream_t st) {
+  if (!idx) return DRS_OK;
+  const IndexDesc d = make_index_desc(M);
+  const size_t bytes = (size_t)(TAB_HDR + 2 * table_tiles(M)) * sizeof(double);
+  return cudaMemsetAsync(idx + d.aoff, 0, bytes, st) == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+}
+
 int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
+  if (write_direct_header(idx, M, st)) return DRS_ERR_LAUNCH;
   if (d.levels == 0) return DRS_OK;
   if (!idx) return DRS_ERR_ARG;
   const int64_t total = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
@@ -483,11 +555,12 @@ int dr_sample_binary(const double* W, const double* idx, int64_t M, uint64_t k0,
   return launch_rc();
 }
 
-int dr_match_ccf(const double* W, int64_t M, const double* U, int64_t N, int64_t* out, void* stream) {
+int dr_match_ccf(const double* W, const double* idx, int64_t M, const double* U, int64_t N, int64_t* out,
+                 void* stream) {
   if (M < 1 || N < 0 || !W || (N > 0 && (!U || !out))) return DRS_ERR_ARG;
   if ((uintptr_t)W & 15) return DRS_ERR_ALIGN;
   if (N == 0) return DRS_OK;
-  return launch_merge(W, M, U, N, out, (cudaStream_t)stream);
+  return launch_merge(W, idx, M, U, N, out, (cudaStream_t)stream);
 }
 
 int dr_match_dac(const double* W, const double* idx, int64_t M, const double* U, int64_t N,
@@ -499,7 +572,7 @@ int dr_match_dac(const double* W, const double* idx, int64_t M, const double* U,
   bool merge = (mode == DRS_DAC_MERGE) || (mode == DRS_DAC_AUTO && M <= DAC_TAU * N);
   if (!merge && make_index_desc(M).levels > 0 && !idx) merge = true;
   cudaStream_t st = (cudaStream_t)stream;
-  if (merge) return launch_merge(W, M, U, N, out, st);
+  if (merge) return launch_merge(W, idx, M, U, N, out, st);
   return launch_index(W, idx, M, U, N, out, st);
 }
 

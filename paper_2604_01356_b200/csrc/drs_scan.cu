@@ -415,6 +415,117 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
   (void)total_out;
 }
 
+// ------------------------------------------- K1 in one pass (deferred) ----
+// dr_build_table_deferred: ONE pass over w.  Each tile's in-tile chained sums
+// L = R + (Q + s) -- k_table_pass2's association without the tile prefix
+// C_g + D_t, which needs every tile before it -- are stored as the table's
+// values, the tile's level-1 index entries likewise, the tile total to
+// agg[t]; validation as in pass 1.  k_chain_groups then folds the tile
+// totals, and k_table_levels stores each tile's pair {C_g, D_t} and T in the
+// index header, turns level 1 into W and writes the levels above it.  Reads
+// w once and writes the table once: 16 bytes per entry instead of 24.
+template <bool LOGW>
+__global__ void __launch_bounds__(THREADS) k_table_local(const double* __restrict__ w, int64_t n, ScanWS ws,
+                                                         double* __restrict__ L, double* __restrict__ lvl1) {
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ FoldSmem fs;
+  constexpr int64_t TS = (int64_t)THREADS * K_TABLE;
+  const int64_t t = blockIdx.x;
+  pdl_wait();
+  const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
+  if (LOGW) exp_shift_tile(sm, len, ws.hdr->wmax);
+  double* chunk = sm + threadIdx.x * K_TABLE;
+  uint32_t any_sign = 0, max_mag = 0;
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < K_TABLE; ++i) {
+    const double x = chunk[i];
+    const uint32_t hi = (uint32_t)__double2hiint(x);
+    any_sign |= hi;
+    max_mag = max(max_mag, hi & 0x7FFFFFFFu);
+    s = (i == 0) ? x : __dadd_rn(s, x);
+  }
+  bool bad = max_mag >= 0x7FF00000u;
+  if (any_sign & 0x80000000u)
+    for (int i = 0; i < K_TABLE; ++i) bad |= !(chunk[i] >= 0.0);
+  double Q, R;
+  const double A = block_fold(s, fs, Q, R);
+  pdl_trigger();
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(&ws.hdr->status, (uint32_t)DRS_ST_INVALID_WEIGHT);
+  if (threadIdx.x == 0) ws.agg[t] = A;
+  double s2 = 0.0;
+#pragma unroll
+  for (int i = 0; i < K_TABLE; ++i) {
+    const double x = chunk[i];
+    s2 = (i == 0) ? x : __dadd_rn(s2, x);
+    chunk[i] = __dadd_rn(R, __dadd_rn(Q, s2));
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  const int64_t len_even = len & ~(int64_t)1;
+  const int64_t j0 = t * TS;
+  if (threadIdx.x == 0) {
+    if (len_even > 0) bulk_s2g(L + j0, sm, (uint32_t)(len_even * 8));
+    if (len & 1) L[j0 + len - 1] = sm[len - 1];
+  }
+  if (lvl1) {  // level 1: the value at every 16-entry block end (the last block ends at n-1)
+    static_assert(TS % FANOUT == 0, "level-1 blocks never straddle table tiles");
+    const int64_t jl = j0 + len - 1;
+    for (int64_t m = j0 / FANOUT + threadIdx.x; m < (jl + 1) / FANOUT; m += THREADS)
+      lvl1[m] = sm[(m + 1) * FANOUT - 1 - j0];
+    if (jl == n - 1 && (n % FANOUT) && threadIdx.x == 0) lvl1[(n - 1) / FANOUT] = sm[len - 1];
+  }
+  if (threadIdx.x == 0 && len_even > 0) bulk_commit_wait();
+}
+
+// after the chain: the table header {T, 1, 0, 0} and the tile pairs; level 1
+// (in-tile values) -> W = min(S / T, 1), W[M-1] = 1, exactly what
+// k_table_pass2 stores; an entry that ends a block of a higher level is
+// stored there too; +inf padding of every level to whole nodes
+__global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, ScanWS ws, double* __restrict__ idx,
+                                                      IndexDesc d) {
+  pdl_wait();
+  pdl_trigger();
+  const double T = ws.hdr->total;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double* aux = idx + d.aoff;
+  if (e < nt) reinterpret_cast<double2*>(aux + TAB_HDR)[e] = make_double2(ws.grp[e / GROUP_TILES], ws.incl[e]);
+  if (e == 0) {
+    aux[0] = T;
+    aux[1] = 1.0;
+    aux[2] = 0.0;
+    aux[3] = 0.0;
+  }
+  if (d.levels == 0) return;
+  if (e < (int64_t)FANOUT * d.levels) {
+    const int k = 1 + (int)(e / FANOUT);
+    const int64_t p = d.n[k] + e % FANOUT;
+    if (p < cdiv(d.n[k], FANOUT) * FANOUT) idx[d.off[k] + p] = dinf();
+  }
+  if (e >= d.n[1]) return;
+  const int64_t p = (e * FANOUT + FANOUT - 1 < M - 1) ? e * FANOUT + FANOUT - 1 : M - 1;
+  const int64_t tt = p / TABLE_TILE;
+  const double S = __dadd_rn(ws.grp[tt / GROUP_TILES], __dadd_rn(ws.incl[tt], idx[d.off[1] + e]));
+  const double v = (p == M - 1) ? 1.0 : fmin(__ddiv_rn(S, T), 1.0);
+  idx[d.off[1] + e] = v;
+  for (int k = 2, sh = 8; k <= d.levels; ++k, sh += 4) {
+    if (p != M - 1 && ((p + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
+    idx[d.off[k] + (p >> sh)] = v;
+  }
+}
+
+// a table's cumulative weights: W itself (direct) or formed (deferred)
+__global__ void __launch_bounds__(256) k_table_materialize(const double* __restrict__ V, int64_t M,
+                                                           const double* __restrict__ aux, double* __restrict__ W) {
+  const TabAux ta = load_aux(aux);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += stride) {
+    const double v = V[j];
+    W[j] = ta.def ? tab_w(ta, __ldg(ta.P + j / TABLE_TILE), v, j == M - 1) : v;
+  }
+}
+
 // ------------------------------------------------- K2 sorted uniforms ----
 __device__ __forceinline__ unsigned long long zmin_key(double z) {
   // positive doubles order like their bit patterns; NaN / <= 0 force the exact check
@@ -583,6 +694,7 @@ IndexDesc make_index_desc(int64_t M) {
   d.kt = 0;
   d.tshift = 0;
   d.toff = 0;
+  d.aoff = 0;
   if (L > 0) {
     int k = 1;
     while (d.n[k] > DRS_TG_ENTRIES) ++k;  // n[L] <= FANOUT, so k <= L
@@ -591,6 +703,7 @@ IndexDesc make_index_desc(int64_t M) {
     d.kt = k;
     d.tshift = sh < 4 ? 4 : sh;
     d.toff = off;
+    d.aoff = off + tg_doubles(d);  // a multiple of 16 doubles
   }
   return d;
 }
@@ -601,18 +714,51 @@ static int launch_rc() {
 }
 
 static void set_attrs() {
-  static SmemLimit l1, l2, l3, l4;
+  static SmemLimit l1, l2, l3, l4, l5, l6;
   const size_t smem = (size_t)THREADS * K_TABLE * 8;
   l1.raise((const void*)k_table_pass1<false>, smem);
   l2.raise((const void*)k_table_pass1<true>, smem);
   l3.raise((const void*)k_table_pass2<false, false>, smem);
   l4.raise((const void*)k_table_pass2<true, false>, smem);
+  l5.raise((const void*)k_table_local<false>, smem);
+  l6.raise((const void*)k_table_local<true>, smem);
 }
 
+int write_direct_header(double* idx, int64_t M, cudaStream_t st);  // drs_match.cu
+
+// dr_build_table_deferred / dr_build_table_log_deferred
+static int build_deferred(const double* w, bool logw, int64_t M, double* L, double* idx, int32_t* status, void* ws,
+                          size_t ws_bytes, cudaStream_t st) {
+  if (M < 1 || !w || !L || !idx || !status || !ws) return DRS_ERR_ARG;
+  if (((uintptr_t)w | (uintptr_t)L | (uintptr_t)idx) & 15) return DRS_ERR_ALIGN;
+  const IndexDesc d = make_index_desc(M);
+  const int64_t nt = cdiv(M, (int64_t)THREADS * K_TABLE);
+  if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
+  set_attrs();
+  const ScanWS s = carve(ws, ws_bytes);
+  const int smem = THREADS * K_TABLE * 8;
+  double* lvl1 = d.levels > 0 ? idx + d.off[1] : nullptr;
+  if (logw) {
+    const int64_t mb = cdiv(M, 256 * 8);
+    const unsigned mgrid = (unsigned)(mb < nt ? (mb < 1 ? 1 : mb) : nt);  // partials fit in agg[nt]
+    launch_pdl(k_max_logw, dim3(mgrid < 1184 ? mgrid : 1184), dim3(256), 0, st, w, M, s);
+    launch_pdl(k_table_local<true>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, L, lvl1);
+  } else {
+    launch_pdl(k_table_local<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, L, lvl1);
+  }
+  launch_chain(s, nt, 0, status, nullptr, st);
+  int64_t work = nt;
+  if (d.levels > 0) work = std::max<int64_t>(work, std::max<int64_t>(d.n[1], (int64_t)FANOUT * d.levels));
+  launch_pdl(k_table_levels, dim3((unsigned)cdiv(work, 256)), dim3(256), 0, st, M, nt, s, idx, d);
+  if (launch_rc()) return DRS_ERR_LAUNCH;
+  return launch_top_guide(M, idx, st);
+}
+
+// levels, top guide, then the table header and the per-tile pairs (TabAux)
 int64_t index_entries(int64_t M) {
   const IndexDesc d = make_index_desc(M);
-  if (d.levels == 0) return 0;
-  return d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT + tg_doubles(d);
+  return d.aoff + TAB_HDR + 2 * table_tiles(M);
 }
 
 int64_t ws_capacity_tiles(size_t ws_bytes) { return ws_tile_capacity(ws_bytes); }
@@ -718,8 +864,26 @@ int dr_build_table(const double* w, int64_t M, double* W, double* idx, int32_t* 
   launch_chain(s, nt, 0, status, nullptr, st);
   launch_pdl(k_table_pass2<false, false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, nt, s, W, idx, d,
              status, (double*)nullptr);
-  if (launch_rc()) return DRS_ERR_LAUNCH;
+  if (launch_rc() || write_direct_header(idx, M, st)) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
+}
+
+int dr_build_table_deferred(const double* w, int64_t M, double* V, double* idx, int32_t* status, void* ws,
+                            size_t ws_bytes, void* stream) {
+  return build_deferred(w, false, M, V, idx, status, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int dr_build_table_log_deferred(const double* logw, int64_t M, double* V, double* idx, int32_t* status, void* ws,
+                                size_t ws_bytes, void* stream) {
+  return build_deferred(logw, true, M, V, idx, status, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int dr_table_materialize(const double* V, const double* idx, int64_t M, double* W, void* stream) {
+  if (M < 1 || !V || !W) return DRS_ERR_ARG;
+  const IndexDesc d = make_index_desc(M);
+  const int64_t blocks = cdiv(M, 256) < 148 * 16 ? cdiv(M, 256) : 148 * 16;
+  k_table_materialize<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(V, M, idx ? idx + d.aoff : nullptr, W);
+  return launch_rc();
 }
 
 int dr_build_table_log(const double* logw, int64_t M, double* W, double* idx, int32_t* status, void* ws,
@@ -742,7 +906,7 @@ int dr_build_table_log(const double* logw, int64_t M, double* W, double* idx, in
   launch_chain(s, nt, 0, status, nullptr, st);
   launch_pdl(k_table_pass2<false, false>, dim3((unsigned)nt), dim3(THREADS), smem, st, (const double*)W, M, nt, s,
              W, idx, d, status, (double*)nullptr);
-  if (launch_rc()) return DRS_ERR_LAUNCH;
+  if (launch_rc() || write_direct_header(idx, M, st)) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
 }
 

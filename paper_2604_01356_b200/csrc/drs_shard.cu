@@ -85,8 +85,9 @@ __global__ void __launch_bounds__(256) k_shard_match(const double* __restrict__ 
   const double* Ug = U - range[4];  // window -> global index
   int64_t* og = out - range[5];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const TabAux ta = load_aux(idx ? idx + d.aoff : nullptr);
   for (int64_t i = a + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < b; i += stride)
-    og[i] = shard_start + index_lower_bound(W, idx, d, __ldg(Ug + i));
+    og[i] = shard_start + index_lower_bound(W, idx, d, ta, __ldg(Ug + i));
 }
 
 // ---------------------------------------------- sharded sorted uniforms ----

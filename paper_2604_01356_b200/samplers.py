@@ -83,7 +83,7 @@ def _lower_bounds(table: WeightTable, u: torch.Tensor) -> torch.Tensor:
     if u.numel():
         _lib.check(
             _lib.lib().dr_match_binary(
-                table.device_cum.data_ptr(), _ptr(table.device_index), table.size,
+                table.device_values.data_ptr(), _ptr(table.device_index), table.size,
                 u.data_ptr(), u.numel(), out.data_ptr(), _lib.stream_handle(),
             ),
             "dr_match_binary",
@@ -137,9 +137,10 @@ def _match(kind: str, u, table: WeightTable, check: bool, mode: str = "auto", st
     if n:
         L = _lib.lib()
         s = _lib.stream_handle()
-        W = table.device_cum
+        W = table.device_values
         if kind == "ccf":
-            rc = L.dr_match_ccf(W.data_ptr(), table.size, ud.data_ptr(), n, out.data_ptr(), s)
+            rc = L.dr_match_ccf(W.data_ptr(), _ptr(table.device_index), table.size, ud.data_ptr(), n,
+                                out.data_ptr(), s)
         else:
             rc = L.dr_match_dac(W.data_ptr(), _ptr(table.device_index), table.size, ud.data_ptr(), n,
                                 out.data_ptr(), _lib.DAC_MODES[mode], s)
@@ -202,7 +203,7 @@ def binary_sampler(table: WeightTable, n: int, stream, stats: OpStats | None = N
     if out is None:
         out = empty_i64(n) if device else host_result_i64(n)
     if n:
-        W = table.device_cum
+        W = table.device_values
         if isinstance(stream, (RngStream, DeviceRngStream)):
             k0, k1, off, offd = _stream_args(stream, n)
             rc = _lib.lib().dr_sample_binary_dev(W.data_ptr(), _ptr(table.device_index), table.size,
@@ -315,7 +316,7 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
     U = _scratch_uniforms(n, s) if U is None else U
     st = _status_buf(s)
     ws, wsb = _lib.workspace(_lib.workspace_bytes(_lib.OP_SORTED, n), s)
-    W = table.device_cum
+    W = table.device_values
     if not isinstance(stream, (RngStream, DeviceRngStream)):
         # duck-typed host stream: its n+1 uniforms feed the same fused kernel
         raw, _ = to_device_f64(stream.uniforms(n + 1))
@@ -327,7 +328,7 @@ def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None
         return out if device else out.cpu().numpy()
     k0, k1, off, offd = _stream_args(stream, n + 1)
     if kind == "ccf":
-        rc = L.dr_sample_ccf(W.data_ptr(), table.size, k0, k1, off, offd, n, U.data_ptr(), out.data_ptr(),
+        rc = L.dr_sample_ccf(W.data_ptr(), _ptr(table.device_index), table.size, k0, k1, off, offd, n, U.data_ptr(), out.data_ptr(),
                              st.data_ptr(), ws, wsb, s)
     else:
         rc = L.dr_sample_dac(W.data_ptr(), _ptr(table.device_index), table.size, k0, k1, off, offd, n,

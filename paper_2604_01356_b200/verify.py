@@ -109,7 +109,7 @@ def resample_and_gather(table: WeightTable, n: int, stream, states, *, divisor: 
         st = _samplers._status_buf(sh)
         ws, wsb = _lib.workspace(_lib.workspace_bytes(_lib.OP_SORTED, n), sh)
         k0, k1, off, offd = _samplers._stream_args(stream, n + 1)
-        _lib.check(L.dr_sample_dac_gather(table.device_cum.data_ptr(), _samplers._ptr(table.device_index),
+        _lib.check(L.dr_sample_dac_gather(table.device_values.data_ptr(), _samplers._ptr(table.device_index),
                                           table.size, k0, k1, off, offd, n, U.data_ptr(), idx.data_ptr(),
                                           s_.data_ptr(), K, d, divisor, rows.data_ptr(), st.data_ptr(),
                                           _lib.DAC_MODES[mode], ws, wsb, sh), "dr_sample_dac_gather")

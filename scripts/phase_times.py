@@ -34,7 +34,7 @@ import bench  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 c = bench.CONFIGS[cfg]
-table = drs.build_weight_table(bench.make_weights(cfg))
+table = drs.build_weight_table(bench.make_weights(cfg), deferred=os.environ.get("DRS_TABLE", "deferred") == "deferred")
 N = c["N"]
 st = drs.RngStream(c["useed"])
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

@@ -157,8 +157,11 @@ def test_build_table_bit_exact_vs_oracle(drs, orc, golden):
         t = drs.build_weight_table(raw)
         W, _ = orc.build_table(raw)
         np.testing.assert_array_equal(t.cum, W)
-        np.testing.assert_array_equal(t.device_index.cpu().numpy() if t.device_index is not None else np.empty(0),
-                                      orc.build_index(W))
+        # the single-pass (deferred) table: values, index, header and tile pairs
+        np.testing.assert_array_equal(t.device_index.cpu().numpy(), orc.build_table_deferred(raw)[1])
+        t2 = drs.build_weight_table(raw, deferred=False)  # the two-pass table
+        np.testing.assert_array_equal(t2.cum, W)
+        np.testing.assert_array_equal(t2.device_index.cpu().numpy(), orc.build_index(W))
         ref = golden[f"tbl_cum_{i}"]
         assert np.abs(t.cum - ref).max() <= 1e-12
 
