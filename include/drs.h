@@ -246,6 +246,18 @@ int dr_shard_finalize(double *S_to_W, int64_t Mg, const double *totals, int32_t 
  * that lands in shard g, as a range8 (layout below) over the full U:
  * range8[0] = #(U <= fl(O_g/T)) (0 for g = 0), range8[1] = #(U <= fl(O_{g+1}/T))
  * (N for the last rank), range8[4] = range8[5] = 0 (U and out are full-length). */
+/* The single-pass shard build (16 bytes per entry): dr_shard_scan_deferred
+ * writes the shard's in-tile sums to V[Mg], its level-1 index entries and
+ * tile pairs to idx[dr_index_entries(Mg)] and its total to *Tg; after the
+ * caller's all-gather of the G totals, dr_shard_finalize_deferred writes the
+ * header {T, 2, O_g, g == G-1} and the index levels of W -- no pass over the
+ * shard's values.  The shard's W (dr_table_materialize) is bit-identical to
+ * dr_shard_finalize's. */
+int dr_shard_scan_deferred(const double *w_shard, int64_t Mg, double *V, double *idx, double *Tg,
+                           int32_t *status, void *ws, size_t ws_bytes, void *stream);
+int dr_shard_finalize_deferred(int64_t Mg, const double *totals, int32_t G, int32_t g, double *idx,
+                               void *stream);
+
 int dr_shard_range(const double *U, int64_t N, const double *totals, int32_t G, int32_t g,
                    int64_t *range8, void *stream);
 /* Step 4: indices of the rank's slice.  range8 (device int64[8]):

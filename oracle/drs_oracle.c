@@ -241,7 +241,7 @@ int drs_ref_build_table(const double *w, int64_t M, double *W) {
  * drs_ref_chain_scan, split at the tile prefix: V[j] = R + (Q + s) (the
  * in-tile sums), per tile the pair {C_g, D_t}, so that S = C_g + (D_t + V[j]);
  * idx = the index of W = min(S / T, 1), W[M-1] = 1 (drs_ref_build_table's W),
- * then the header {T, 1, 0, 0} and the pairs.  W may be NULL. */
+ * then the header {T, 1, 0, 1} and the pairs.  W may be NULL. */
 int drs_ref_build_table_deferred(const double *w, int64_t M, double *V, double *idx, double *Wout) {
   const int K = DRS_REF_K_TABLE;
   const int64_t TS = DRS_REF_TABLE_TILE;
@@ -288,9 +288,9 @@ int drs_ref_build_table_deferred(const double *w, int64_t M, double *V, double *
   drs_ref_build_index(W, M, idx);
   double *aux = idx + drs_ref_search_entries(M);
   aux[0] = T;
-  aux[1] = 1.0;
-  aux[2] = 0.0;
-  aux[3] = 0.0;
+  aux[1] = 1.0; /* mode 1: S = C + (D + V) */
+  aux[2] = 0.0; /* O (shards only) */
+  aux[3] = 1.0; /* the last entry pinned to 1 */
   memcpy(aux + 4, P, sizeof(double) * 2 * (size_t)nt);
   if (Wout) memcpy(Wout, W, sizeof(double) * (size_t)M);
   free(P);

@@ -78,6 +78,9 @@ _PROTOS = {
     "dr_resample_batched": (_int, [_c_void_p, _i64, _i64, _i64, _c_void_p, _i32, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "dr_shard_scan": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "dr_shard_finalize": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
+    "dr_shard_scan_deferred": (_int, [_c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size,
+                                      _c_void_p]),
+    "dr_shard_finalize_deferred": (_int, [_i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
     "dr_shard_range": (_int, [_c_void_p, _i64, _c_void_p, _i32, _i32, _c_void_p, _c_void_p]),
     "dr_shard_unif_totals": (_int, [_u64, _u64, _u64, _i64, _i64, _i64, _c_void_p, _c_void_p, _c_void_p]),
     "dr_shard_unif_local": (_int, [_u64, _u64, _u64, _i64, _c_void_p, _c_void_p, _i64, _c_void_p, _i32, _i32,

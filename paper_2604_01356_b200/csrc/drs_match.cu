@@ -125,7 +125,7 @@ __device__ __forceinline__ void stage_to_w(double* sw, int len, int64_t j0, int6
   const DivBy byT = div_by(ta.T);
   for (int i = threadIdx.x; i < len; i += blockDim.x) {
     const double2 cd = __ldg(P + (i < jb ? 0 : 1));
-    sw[i] = (i == il) ? 1.0 : fmin(div_rn(__dadd_rn(cd.x, __dadd_rn(cd.y, sw[i])), byT), 1.0);
+    sw[i] = (i == il && ta.pin) ? 1.0 : fmin(div_rn(tab_sum(ta, cd, sw[i]), byT), 1.0);
   }
 }
 
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
   __shared__ __align__(8) uint64_t bar;
   __shared__ int64_t s_ib, s_ie;
   __shared__ int s_w0, s_w1;
-  __shared__ double2 s_hdr;  // the table header {T, deferred}, read beside the u-run searches
+  __shared__ double2 s_hdr, s_hdr2;  // the table header {T, mode}, {O, pin}, read beside the u-run searches
   __shared__ double2 s_pair[2];  // a deferred table's tile pairs around j0
   __shared__ int s_probe;        // deferred, few u's: W formed at each bisection probe
   const int64_t t = blockIdx.x;
@@ -175,7 +175,10 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
   if (threadIdx.x >= 96 && threadIdx.x < 99) {
     // the table header and a deferred table's tile pairs around j0 (unused,
     // all zero, for a direct table), loaded beside the u-run searches
-    if (threadIdx.x == 96) s_hdr = aux ? __ldg(reinterpret_cast<const double2*>(aux)) : make_double2(1.0, 0.0);
+    if (threadIdx.x == 96) {
+      s_hdr = aux ? __ldg(reinterpret_cast<const double2*>(aux)) : make_double2(1.0, 0.0);
+      s_hdr2 = aux ? __ldg(reinterpret_cast<const double2*>(aux) + 1) : make_double2(0.0, 1.0);
+    }
     else if (aux) s_pair[threadIdx.x - 97] = __ldg(reinterpret_cast<const double2*>(aux + TAB_HDR) +
                                                    min(j0 / TABLE_TILE + (threadIdx.x - 97), table_tiles(M) - 1));
     s_probe = 0;
@@ -219,8 +222,9 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             const double2 cd = s_pair[mid < jb ? 0 : 1];
-            const double v = (j0 + mid == M - 1)
-                                 ? 1.0 : fmin(__ddiv_rn(__dadd_rn(cd.x, __dadd_rn(cd.y, sw[mid])), s_hdr.x), 1.0);
+            double S = __dadd_rn(cd.x, __dadd_rn(cd.y, sw[mid]));
+            if (s_hdr.y == 2.0) S = __dadd_rn(s_hdr2.x, S);  // a shard of a W-sharded table
+            const double v = (j0 + mid == M - 1 && s_hdr2.y != 0.0) ? 1.0 : fmin(__ddiv_rn(S, s_hdr.x), 1.0);
             if (v < x) lo = mid + 1;
             else hi = mid;
           }

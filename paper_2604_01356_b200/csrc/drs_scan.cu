@@ -432,8 +432,11 @@ __global__ void __launch_bounds__(THREADS) k_table_local(const double* __restric
   __shared__ FoldSmem fs;
   constexpr int64_t TS = (int64_t)THREADS * K_TABLE;
   const int64_t t = blockIdx.x;
+  STAMPK(4, 0);
   pdl_wait();
+  STAMPK(4, 1);
   const int64_t len = stage_tile<K_TABLE>(w, n, t, sm, &bar);
+  STAMPK(4, 2);
   if (LOGW) exp_shift_tile(sm, len, ws.hdr->wmax);
   double* chunk = sm + threadIdx.x * K_TABLE;
   uint32_t any_sign = 0, max_mag = 0;
@@ -477,42 +480,90 @@ __global__ void __launch_bounds__(THREADS) k_table_local(const double* __restric
     if (jl == n - 1 && (n % FANOUT) && threadIdx.x == 0) lvl1[(n - 1) / FANOUT] = sm[len - 1];
   }
   if (threadIdx.x == 0 && len_even > 0) bulk_commit_wait();
+  STAMPK(4, 3);
 }
 
-// after the chain: the table header {T, 1, 0, 0} and the tile pairs; level 1
-// (in-tile values) -> W = min(S / T, 1), W[M-1] = 1, exactly what
-// k_table_pass2 stores; an entry that ends a block of a higher level is
-// stored there too; +inf padding of every level to whole nodes
+// after the chain: level 1 (in-tile values) -> W = min(S / T, 1), the last
+// entry pinned to 1, exactly what k_table_pass2 / k_shard_finalize store; an
+// entry that ends a block of a higher level is stored there too; +inf padding
+// of every level to whole nodes.  FROM_WS (dr_build_table_deferred): the tile
+// pairs come from the chain's workspace and are stored with the header
+// {T, 1, 0, 1}; otherwise (a shard: dr_shard_finalize_deferred) the header and
+// pairs are already in idx.  A persistent grid, two level-1 entries per
+// thread per step (16-byte accesses), the division by T as a multiply and two
+// FMAs (div_rn, bit-identical).
+template <bool FROM_WS>
 __global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, ScanWS ws, double* __restrict__ idx,
                                                       IndexDesc d) {
+  STAMPK(5, 0);
   pdl_wait();
+  STAMPK(5, 1);
   pdl_trigger();
-  const double T = ws.hdr->total;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   double* aux = idx + d.aoff;
-  if (e < nt) reinterpret_cast<double2*>(aux + TAB_HDR)[e] = make_double2(ws.grp[e / GROUP_TILES], ws.incl[e]);
-  if (e == 0) {
-    aux[0] = T;
-    aux[1] = 1.0;
-    aux[2] = 0.0;
-    aux[3] = 0.0;
+  const double2* P = reinterpret_cast<const double2*>(aux + TAB_HDR);
+  const int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double T, O = 0.0;
+  bool shard = false, pin = true;
+  if (FROM_WS) {
+    T = ws.hdr->total;
+    for (int64_t e = e0; e < nt; e += stride)
+      reinterpret_cast<double2*>(aux + TAB_HDR)[e] = make_double2(ws.grp[e / GROUP_TILES], ws.incl[e]);
+    if (e0 == 0) {
+      aux[0] = T;
+      aux[1] = 1.0;
+      aux[2] = 0.0;
+      aux[3] = 1.0;
+    }
+  } else {
+    const TabAux ta = load_aux(aux);
+    T = ta.T;
+    O = ta.O;
+    shard = ta.shard;
+    pin = ta.pin;
   }
   if (d.levels == 0) return;
-  if (e < (int64_t)FANOUT * d.levels) {
-    const int k = 1 + (int)(e / FANOUT);
-    const int64_t p = d.n[k] + e % FANOUT;
+  if (e0 < (int64_t)FANOUT * d.levels) {
+    const int k = 1 + (int)(e0 / FANOUT);
+    const int64_t p = d.n[k] + e0 % FANOUT;
     if (p < cdiv(d.n[k], FANOUT) * FANOUT) idx[d.off[k] + p] = dinf();
   }
-  if (e >= d.n[1]) return;
-  const int64_t p = (e * FANOUT + FANOUT - 1 < M - 1) ? e * FANOUT + FANOUT - 1 : M - 1;
-  const int64_t tt = p / TABLE_TILE;
-  const double S = __dadd_rn(ws.grp[tt / GROUP_TILES], __dadd_rn(ws.incl[tt], idx[d.off[1] + e]));
-  const double v = (p == M - 1) ? 1.0 : fmin(__ddiv_rn(S, T), 1.0);
-  idx[d.off[1] + e] = v;
-  for (int k = 2, sh = 8; k <= d.levels; ++k, sh += 4) {
-    if (p != M - 1 && ((p + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
-    idx[d.off[k] + (p >> sh)] = v;
+  const DivBy byT = div_by(T);
+  const int64_t n1 = d.n[1];  // level 1 starts at offset 0 (16-byte aligned)
+  for (int64_t e = 2 * e0; e < n1; e += 2 * stride) {
+    const bool two = e + 1 < n1;
+    double2 l;
+    if (two) l = *reinterpret_cast<const double2*>(idx + e);
+    else l = make_double2(idx[e], 0.0);
+    double v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t m = e + h;
+      const int64_t p = (m * FANOUT + FANOUT - 1 < M - 1) ? m * FANOUT + FANOUT - 1 : M - 1;
+      const int64_t tt = p / TABLE_TILE;
+      const double2 cd = FROM_WS ? make_double2(ws.grp[tt / GROUP_TILES], ws.incl[tt]) : __ldg(P + tt);
+      const double sl = __dadd_rn(cd.x, __dadd_rn(cd.y, h ? l.y : l.x));
+      const double S = shard ? __dadd_rn(O, sl) : sl;
+      v[h] = (p == M - 1 && pin) ? 1.0 : fmin(div_rn(S, byT), 1.0);
+      if (m >= n1) continue;
+      for (int k = 2, sh = 8; k <= d.levels; ++k, sh += 4) {
+        if (p != M - 1 && ((p + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
+        idx[d.off[k] + (p >> sh)] = v[h];
+      }
+    }
+    if (two) *reinterpret_cast<double2*>(idx + e) = make_double2(v[0], v[1]);
+    else idx[e] = v[0];
   }
+}
+
+// a shard's scan (dr_shard_scan_deferred): the tile pairs from the chain's
+// workspace into idx (the header follows once the shard totals are known)
+__global__ void k_table_pairs(int64_t nt, ScanWS ws, double* __restrict__ aux) {
+  pdl_wait();
+  pdl_trigger();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nt; e += stride)
+    reinterpret_cast<double2*>(aux + TAB_HDR)[e] = make_double2(ws.grp[e / GROUP_TILES], ws.incl[e]);
 }
 
 // a table's cumulative weights: W itself (direct) or formed (deferred)
@@ -749,8 +800,9 @@ static int build_deferred(const double* w, bool logw, int64_t M, double* L, doub
   }
   launch_chain(s, nt, 0, status, nullptr, st);
   int64_t work = nt;
-  if (d.levels > 0) work = std::max<int64_t>(work, std::max<int64_t>(d.n[1], (int64_t)FANOUT * d.levels));
-  launch_pdl(k_table_levels, dim3((unsigned)cdiv(work, 256)), dim3(256), 0, st, M, nt, s, idx, d);
+  if (d.levels > 0) work = std::max<int64_t>(work, std::max<int64_t>(cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels));
+  const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * 8);
+  launch_pdl(k_table_levels<true>, dim3((unsigned)lgrid), dim3(256), 0, st, M, nt, s, idx, d);
   if (launch_rc()) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
 }
@@ -789,6 +841,18 @@ int sorted_uniforms_from_launch(const double* raw, int64_t n, double* U, int32_t
                                 size_t ws_bytes, cudaStream_t st) {
   ArraySpacings src{raw};
   return sorted_impl(src, n, U, status, ws, ws_bytes, nullptr, st);
+}
+
+// the levels of a shard whose header is in place (dr_shard_finalize_deferred, drs_shard.cu)
+int launch_table_levels_from_aux(int64_t M, double* idx, cudaStream_t st) {
+  const IndexDesc d = make_index_desc(M);
+  const ScanWS none{};
+  int64_t work = 1;
+  if (d.levels > 0) work = std::max<int64_t>(cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels);
+  const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * 8);
+  launch_pdl(k_table_levels<false>, dim3((unsigned)lgrid), dim3(256), 0, st, M, (int64_t)0, none, idx, d);
+  if (launch_rc()) return DRS_ERR_LAUNCH;
+  return launch_top_guide(M, idx, st);
 }
 
 }  // namespace drs
@@ -926,6 +990,26 @@ int dr_shard_scan(const double* w_shard, int64_t Mg, double* S, double* Tg, int3
   launch_chain(s, nt, 0, status, Tg, st);
   launch_pdl(k_table_pass2<true, false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w_shard, Mg, nt, s, S,
              (double*)nullptr, d, status, Tg);
+  return launch_rc();
+}
+
+int dr_shard_scan_deferred(const double* w_shard, int64_t Mg, double* V, double* idx, double* Tg, int32_t* status,
+                           void* ws, size_t ws_bytes, void* stream) {
+  if (Mg < 1 || !w_shard || !V || !idx || !Tg || !status || !ws) return DRS_ERR_ARG;
+  if (((uintptr_t)w_shard | (uintptr_t)V | (uintptr_t)idx) & 15) return DRS_ERR_ALIGN;
+  const IndexDesc d = make_index_desc(Mg);
+  const int64_t nt = cdiv(Mg, (int64_t)THREADS * K_TABLE);
+  if (nt > ws_tile_capacity(ws_bytes)) return DRS_ERR_WORKSPACE;
+  if (nt > (int64_t)CHAIN_MAX_GROUPS * GROUP_TILES) return DRS_ERR_ARG;
+  set_attrs();
+  const ScanWS s = carve(ws, ws_bytes);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int smem = THREADS * K_TABLE * 8;
+  launch_pdl(k_table_local<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w_shard, Mg, s, V,
+             d.levels > 0 ? idx + d.off[1] : (double*)nullptr);
+  launch_chain(s, nt, 0, status, Tg, st);
+  launch_pdl(k_table_pairs, dim3((unsigned)std::min<int64_t>(cdiv(nt, 256), 1184)), dim3(256), 0, st, nt, s,
+             idx + d.aoff);
   return launch_rc();
 }
 

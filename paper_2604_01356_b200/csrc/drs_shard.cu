@@ -13,6 +13,7 @@ namespace drs {
 
 IndexDesc make_index_desc(int64_t M);
 int launch_build_index(const double* W, int64_t M, double* idx, cudaStream_t st);
+int launch_table_levels_from_aux(int64_t M, double* idx, cudaStream_t st);  // drs_scan.cu
 int launch_index_sm(const double* W, const double* idx, int64_t M, const double* u, int64_t N, int64_t* out,
                     cudaStream_t st, const int64_t* rng, int64_t shift);
 void launch_chain(const ScanWS& s, int64_t nt, int mode, int32_t* status, double* total, cudaStream_t st);
@@ -42,6 +43,17 @@ __global__ void k_shard_finalize(double* __restrict__ S, int64_t Mg, const doubl
     if (g == G - 1 && j == Mg - 1) v = 1.0;
     S[j] = v;
   }
+}
+
+// the header of a deferred shard {T, 2, O_g, pin}: S = O_g + (C + (D + L)),
+// W = min(S / T, 1), only the last shard's last entry pinned to 1
+__global__ void k_shard_header(const double* __restrict__ totals, int G, int g, double* __restrict__ aux) {
+  double Og, Og1, T;
+  fold_offsets(totals, G, g, Og, Og1, T);
+  aux[0] = T;
+  aux[1] = 2.0;
+  aux[2] = Og;
+  aux[3] = (g == G - 1) ? 1.0 : 0.0;
 }
 
 __device__ __forceinline__ int64_t warp_count_le_s(const double* __restrict__ U, int64_t N, double key) {
@@ -310,6 +322,15 @@ int dr_shard_finalize(double* S_to_W, int64_t Mg, const double* totals, int32_t 
   k_shard_finalize<<<(unsigned)blocks, 256, 0, st>>>(S_to_W, Mg, totals, G, g);
   if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
   return launch_build_index(S_to_W, Mg, idx, st);
+}
+
+int dr_shard_finalize_deferred(int64_t Mg, const double* totals, int32_t G, int32_t g, double* idx,
+                               void* stream) {
+  if (Mg < 1 || !totals || !idx || G < 1 || g < 0 || g >= G) return DRS_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_shard_header<<<1, 1, 0, st>>>(totals, G, g, idx + make_index_desc(Mg).aoff);
+  if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
+  return launch_table_levels_from_aux(Mg, idx, st);
 }
 
 int dr_shard_range(const double* U, int64_t N, const double* totals, int32_t G, int32_t g,

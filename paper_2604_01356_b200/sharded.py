@@ -57,29 +57,43 @@ class DeviceShardOps:
     def device(self):
         return self._lib.device()
 
+    deferred = True  # the shards are single-pass (deferred) tables
+
     def shard_scan(self, w: torch.Tensor):
+        """(scan, T_g, status): the shard's single pass (dr_shard_scan_deferred):
+        in-tile sums, level-1 index entries and tile pairs, local total."""
         m = w.numel()
-        S = torch.empty(m, dtype=torch.float64, device=w.device)
         Tg = torch.zeros(1, dtype=torch.float64, device=w.device)
         st = torch.zeros(1, dtype=torch.int32, device=w.device)
         if m == 0:  # an empty shard owns no weights: total 0, no error of its own
-            return S, Tg, st
+            return _ShardScan(torch.empty(0, dtype=torch.float64, device=w.device), None), Tg, st
         L = self._lib.lib()
+        V = torch.empty(m, dtype=torch.float64, device=w.device)
+        idx = torch.empty(int(L.dr_index_entries(m)), dtype=torch.float64, device=w.device)
         ws, wsb = self._lib.workspace(L.dr_workspace_bytes(self._lib.OP_TABLE, m, 0, 0))
-        self._lib.check(L.dr_shard_scan(w.data_ptr(), m, S.data_ptr(), Tg.data_ptr(), st.data_ptr(), ws, wsb,
-                                        self._lib.stream_handle()), "dr_shard_scan")
-        return S, Tg, st
+        self._lib.check(L.dr_shard_scan_deferred(w.data_ptr(), m, V.data_ptr(), idx.data_ptr(), Tg.data_ptr(),
+                                                 st.data_ptr(), ws, wsb, self._lib.stream_handle()),
+                        "dr_shard_scan_deferred")
+        return _ShardScan(V, idx), Tg, st
 
-    def finalize(self, S: torch.Tensor, totals: torch.Tensor, G: int, g: int):
+    def finalize(self, S, totals: torch.Tensor, G: int, g: int):
+        """(values, index) of the shard once the totals are known: the header
+        {T, 2, O_g, pin} and the index levels of W (dr_shard_finalize_deferred)."""
         if S.numel() == 0:
-            return S, None
-        L = self._lib.lib()
-        n = int(L.dr_index_entries(S.numel()))
-        idx = torch.empty(n, dtype=torch.float64, device=S.device) if n else None
-        self._lib.check(L.dr_shard_finalize(S.data_ptr(), S.numel(), totals.data_ptr(), G, g,
-                                            0 if idx is None else idx.data_ptr(), self._lib.stream_handle()),
-                        "dr_shard_finalize")
-        return S, idx
+            return S.V, None
+        self._lib.check(self._lib.lib().dr_shard_finalize_deferred(S.numel(), totals.data_ptr(), G, g,
+                                                                   S.idx.data_ptr(), self._lib.stream_handle()),
+                        "dr_shard_finalize_deferred")
+        return S.V, S.idx
+
+    def materialize(self, V: torch.Tensor, idx: torch.Tensor | None) -> torch.Tensor:
+        """The shard's cumulative weights W (dr_table_materialize)."""
+        if V.numel() == 0 or idx is None:
+            return V
+        W = torch.empty_like(V)
+        self._lib.check(self._lib.lib().dr_table_materialize(V.data_ptr(), idx.data_ptr(), V.numel(), W.data_ptr(),
+                                                             self._lib.stream_handle()), "dr_table_materialize")
+        return W
 
     def tile_size(self) -> int:
         lanes, warps, _, k_unif, _, _ = self._lib.scan_geometry()
@@ -123,18 +137,41 @@ class DeviceShardOps:
         return out
 
 
+class _ShardScan:
+    """A shard after its scan: the value array and the index buffer the scan
+    wrote into (level 1 and the tile pairs), until finalize completes them."""
+
+    def __init__(self, V: torch.Tensor, idx: torch.Tensor | None):
+        self.V, self.idx = V, idx
+
+    def numel(self) -> int:
+        return self.V.numel()
+
+    @property
+    def device(self):
+        return self.V.device
+
+
 @dataclass
 class ShardedWeightTable:
     """This rank's shard of a table spread over a process group."""
 
-    W: torch.Tensor            # normalised cumulative weights of the shard
-    index: torch.Tensor | None  # search index of the shard
+    W: torch.Tensor            # the shard's value array (W itself, or a deferred shard's in-tile sums)
+    index: torch.Tensor | None  # search index of the shard (its header tells which)
     totals: torch.Tensor       # all shard totals, rank order (device)
     sizes: list[int]           # all shard sizes
     rank: int
     world: int
     group: object = None
     totals_host: list[float] = field(default_factory=list)  # the same totals on the host
+    deferred: bool = False     # W holds a deferred shard's values (DeviceShardOps)
+
+    @property
+    def cum(self) -> torch.Tensor:
+        """The shard's cumulative weights (formed on the device for a deferred shard)."""
+        if not self.deferred or self.index is None or self.W.numel() == 0:
+            return self.W
+        return DeviceShardOps().materialize(self.W, self.index)
 
     @property
     def start(self) -> int:
@@ -222,7 +259,7 @@ def build_sharded_table(raw_shard, *, group=None, ops=None) -> ShardedWeightTabl
     _raise_build_status(st_glob)
     W, idx = ops.finalize(S, totals, G, g)
     return ShardedWeightTable(W=W, index=idx, totals=totals, sizes=sizes, rank=g, world=G, group=group,
-                              totals_host=totals_host)
+                              totals_host=totals_host, deferred=bool(getattr(ops, "deferred", False)))
 
 
 def _key_and_take(stream, k: int):

@@ -41,7 +41,7 @@ sampler = sys.argv[2] if len(sys.argv) > 2 else "dac"
 mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
 c = bench.CONFIGS[cfg]
 L = _lib.lib()
-TUS = {"scan": ["pass1", "chain", "pass2", "finalize", "k4", "k5", "k6", "k7"],
+TUS = {"scan": ["pass1", "chain", "pass2", "finalize", "table_local", "table_levels", "k6", "k7"],
        "match": ["k0", "k1", "k2", "k3", "merge_tiles", "merge_heavy", "k6", "k7"],
        "": ["k0", "k1", "k2", "k3", "k4", "k5", "k6", "k7"]}
 for tu in TUS:
@@ -49,10 +49,14 @@ for tu in TUS:
     getattr(L, f"dr_debug_phase_times{sfx}").argtypes = [ctypes.c_void_p, ctypes.c_int]
 table = drs.build_weight_table(bench.make_weights(cfg))
 N = c["N"]
-fn = {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}[sampler]
+if sampler == "table":  # K1 (build_weight_table, single pass) from device weights
+    w_dev = torch.from_numpy(bench.make_weights(cfg)).cuda()
+    fn = lambda table, N, st, device, out, **kw: drs.build_weight_table(w_dev, check=False)  # noqa: E731
+else:
+    fn = {"dac": drs.dac_sampler, "ccf": drs.ccf_sampler, "binary": drs.binary_sampler}[sampler]
 kw = {"mode": mode} if sampler == "dac" else {}
 out = torch.empty(N, dtype=torch.int64, device="cuda")
-if sampler != "binary":
+if sampler not in ("binary", "table"):
     kw["uniforms_out"] = torch.empty(N, dtype=torch.float64, device="cuda")
 st = drs.RngStream(c["useed"])
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")

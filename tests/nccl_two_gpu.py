@@ -28,7 +28,7 @@ def main():
     a, b = M * rank // world, M * (rank + 1) // world
     table = drs.build_sharded_table(torch.from_numpy(w[a:b]).cuda())
     Wo, To, _ = orc.build_table_sharded(w, world)
-    np.testing.assert_array_equal(table.W.cpu().numpy(), Wo[a:b])
+    np.testing.assert_array_equal(table.cum.cpu().numpy(), Wo[a:b])
     k0, k1 = orc.key_of(2005)
     Uo, _ = orc.sorted_uniforms(k0, k1, 0, N)
     expect = orc.match("dac", Wo, Uo)

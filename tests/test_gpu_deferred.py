@@ -2,13 +2,14 @@
 
 ``build_weight_table`` stores the in-tile chained sums L and the tile pairs
 {C_g, D_t} (``dr_build_table_deferred``, include/drs.h); a search compares
-S = C_g + (D_t + L) with s*(u), the least double s with fl(s / T) >= u.  These
-tests pin (1) the deferred table's arrays bit for bit against the oracle twin
+S = C_g + (D_t + L) with a band around u T and forms fl(S / T) inside it, a
+merge tile is turned into W (or W is formed at each probe).  These tests pin
+(1) the deferred table's arrays bit for bit against the oracle twin
 (``oracle.build_table_deferred``), (2) its cumulative weights against the
 two-pass build and the oracle's W, and (3) every matcher and sampler on it
 against the same call on the two-pass table, with uniforms placed exactly on,
-one ulp below and one ulp above table values -- where S < s*(u) must agree
-with W < u (reference semantics: samplers.py:81-90, strict < lower bound).
+one ulp below and one ulp above table values -- where the comparison must
+agree with W < u (reference semantics: samplers.py:81-90, strict < lower bound).
 """
 
 import numpy as np
@@ -154,3 +155,34 @@ def test_deferred_table_errors(drs):
             drs.build_weight_table(bad)
     with pytest.raises(ValueError, match="accumulation overflow"):
         drs.build_weight_table([1e308, 1e308])
+
+
+@pytest.mark.parametrize("M,G", [(20, 3), (300_001, 3), ((1 << 20) + 5, 4)])
+def test_sharded_deferred_shards(drs, orc, M, G):
+    """The single-pass shard build (dr_shard_scan_deferred + _finalize_deferred,
+    header mode 2: S = O_g + (C + (D + L))): every shard's W == the oracle's
+    sharded table, its index == the index of that W, and the matchers on the
+    shard's values agree with the oracle on u's placed on its W values."""
+    from paper_2604_01356_b200.cdf import WeightTable
+    from paper_2604_01356_b200.sharded import DeviceShardOps
+
+    ops = DeviceShardOps()
+    w = _weights(M, M + G)
+    cuts = [M * g // G for g in range(G + 1)]
+    scans = [ops.shard_scan(torch.from_numpy(w[cuts[g]:cuts[g + 1]]).cuda()) for g in range(G)]
+    totals = torch.cat([s[1] for s in scans])
+    Wo, To, st = orc.build_table_sharded(w, G)
+    np.testing.assert_array_equal(totals.cpu().numpy(), To)
+    for g in range(G):
+        V, idx = ops.finalize(scans[g][0], totals, G, g)
+        Wg = Wo[cuts[g]:cuts[g + 1]]
+        np.testing.assert_array_equal(ops.materialize(V, idx).cpu().numpy(), Wg)
+        ns = orc.search_entries(Wg.size)
+        np.testing.assert_array_equal(idx.cpu().numpy()[:ns], orc.build_index(Wg)[:ns])
+        t = WeightTable(None, _built=(V, idx, True))
+        u = _boundary_u(Wg, np.random.default_rng(g))
+        u = u[u <= Wg[-1]]
+        expect = orc.match("ccf", Wg, u)
+        for mode in ("merge", "search"):
+            np.testing.assert_array_equal(drs.dac_match(u, t, mode=mode), expect)
+        np.testing.assert_array_equal(drs.ccf_match(u, t), expect)

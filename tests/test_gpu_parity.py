@@ -462,7 +462,7 @@ def _shard_emulation(orc, w, N, key, off, Gs):
         Ws, prev = [], 0
         for g in range(G):
             W, idx = ops.finalize(scans[g][0], totals, G, g)
-            Ws.append(W.cpu().numpy())
+            Ws.append(ops.materialize(W, idx).cpu().numpy())
             tab = ShardedWeightTable(W=W, index=idx, totals=totals, sizes=[p.numel() for p in parts], rank=g,
                                      world=G, totals_host=totals.cpu().tolist())
             ucap, ocap = slice_capacity(tab, N, ts)

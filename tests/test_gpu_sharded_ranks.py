@@ -59,7 +59,7 @@ def _worker(rank, world, port, M, N, mode, q):
         for comm in ("allgather", "none"):
             out, rng = drs.sharded_dac_sampler(table, N, drs.RngStream(2005), gather=True, comm=comm)
             outs.append(out.cpu().numpy())
-        q.put((rank, "ok", (table.W.cpu().numpy(), outs)))
+        q.put((rank, "ok", (table.cum.cpu().numpy(), outs)))
     except Exception as e:  # reported to the parent, which fails the test
         q.put((rank, "error", repr(e)))
     finally:
