@@ -204,7 +204,7 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         e2e_h2d, e2e_d2h = 8 * B * Mf, 8 * B * Nf + 4
     elif cfg == "c5" and world > 1:
         w_host = make_weights(cfg, rank, world)
-        table = drs.build_sharded_table(torch.from_numpy(w_host).to(dev))
+        table = drs.build_sharded_table(torch.from_numpy(w_host).to(dev), deferred=args.table == "deferred")
         N = c["N"]
         stream = drs.RngStream(c["useed"])
         alg_bytes = (8 * c["M"]) // world + 16 * N // world
@@ -350,6 +350,38 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
     # ---- K1 on its own: build_weight_table from device-resident raw weights
     # (16 M algorithmic bytes -- read w, write W)
     table_build = None
+    if not light and cfg == "c5" and world > 1:
+        # the sharded table's build (the public collective call: local scan,
+        # the 24-byte-per-rank all-gather, finalize), both kinds of shard;
+        # max over ranks
+        w_dev = torch.from_numpy(w_host).to(dev)
+        sb = {}
+        for kind in ("deferred", "two-pass"):
+            drs.build_sharded_table(w_dev, deferred=kind == "deferred")
+            ms = []
+            for _ in range(max(3, min(args.steps, 10))):
+                l2_flush()
+                barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                drs.build_sharded_table(w_dev, deferred=kind == "deferred")
+                b.record(s)
+                torch.cuda.synchronize()
+                ms.append(a.elapsed_time(b))
+            t = torch.tensor([statistics.median(ms)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sb[kind] = float(t.item())
+        del w_dev
+        Mg = w_host.size
+        table_build = {"ms": sb["deferred"], "two_pass_ms": sb["two-pass"], "per_rank_entries": Mg,
+                       "GB/s_per_rank": 16 * Mg / (sb["deferred"] * 1e-3) / 1e9,
+                       "frac": 16 * Mg / (sb["deferred"] * 1e-3) / 1e9 / peak_hbm()[0],
+                       "timed": "build_sharded_table (public call incl. the all-gather of the shard totals), "
+                                "max over ranks, CUDA events, L2 flushed",
+                       "note": "deferred shards: dr_shard_scan_deferred + all-gather + dr_shard_finalize_deferred "
+                               "(16 B/entry, no pass after the collective); two_pass: dr_shard_scan + "
+                               "dr_shard_finalize (48 B/entry); the sampled table is --table"}
     if not light and (cfg in ("c1", "c2", "c3") or (cfg == "c5" and world == 1)):
         w_dev = torch.from_numpy(w_host).to(dev)
         from paper_2604_01356_b200 import _lib as dlib

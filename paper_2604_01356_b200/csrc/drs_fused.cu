@@ -178,23 +178,19 @@ __device__ __forceinline__ int count_lt16_half(const double* p, double x) {
   return c;
 }
 
-// the same on a W line of a deferred table: S_j against the key (band test
-// of tab_wkey, the exact quotient inside the band)
-__device__ __forceinline__ bool w_below(const TabAux& ta, double S, double x, const WKey& k) {
-  if (S < k.lo) return true;
-  if (S > k.hi || !(S >= k.lo)) return false;  // above the band, or NaN key
-  return __ddiv_rn(S, ta.T) < x;
-}
+// the same on a W line of a deferred table: its values against the band of
+// the line's tile (tab_lband), the exact quotient inside the band
 __device__ __forceinline__ int count_w16_half(const double* p, const TabAux& ta, double2 cd, double x, const WKey& k) {
   if (!ta.def) return count_lt16_half(p, x);
-  const bool up = w_below(ta, tab_sum(ta, cd, __ldg(p + 7)), x, k);
+  const LBand b = tab_lband(ta, k, cd);
+  const bool up = tab_below(ta, cd, __ldg(p + 7), x, b);
   const double* h = p + (up ? 8 : 0);
   double v[8];
   ldg256(h + 0, v[0], v[1], v[2], v[3]);
   ldg256(h + 4, v[4], v[5], v[6], v[7]);
   int c = up ? 8 : 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) c += w_below(ta, tab_sum(ta, cd, v[i]), x, k) ? 1 : 0;
+  for (int i = 0; i < 8; ++i) c += tab_below(ta, cd, v[i], x, b) ? 1 : 0;
   return c;
 }
 

@@ -49,19 +49,21 @@ ST_SHARD_WINDOW = 0x400
 class DeviceShardOps:
     """The CUDA implementation of the shard steps (libdrs.so)."""
 
-    def __init__(self):
+    def __init__(self, deferred: bool = True):
         from . import _lib
 
         self._lib = _lib
+        # deferred: single-pass shards (16 bytes per entry, no pass after the
+        # all-gather); else the two-pass shards holding W itself
+        self.deferred = deferred
 
     def device(self):
         return self._lib.device()
 
-    deferred = True  # the shards are single-pass (deferred) tables
-
     def shard_scan(self, w: torch.Tensor):
-        """(scan, T_g, status): the shard's single pass (dr_shard_scan_deferred):
-        in-tile sums, level-1 index entries and tile pairs, local total."""
+        """(scan, T_g, status): the shard's single pass (dr_shard_scan_deferred:
+        in-tile sums, level-1 index entries and tile pairs) or its two-pass local
+        chained prefix (dr_shard_scan), and the local total."""
         m = w.numel()
         Tg = torch.zeros(1, dtype=torch.float64, device=w.device)
         st = torch.zeros(1, dtype=torch.int32, device=w.device)
@@ -71,19 +73,28 @@ class DeviceShardOps:
         V = torch.empty(m, dtype=torch.float64, device=w.device)
         idx = torch.empty(int(L.dr_index_entries(m)), dtype=torch.float64, device=w.device)
         ws, wsb = self._lib.workspace(L.dr_workspace_bytes(self._lib.OP_TABLE, m, 0, 0))
-        self._lib.check(L.dr_shard_scan_deferred(w.data_ptr(), m, V.data_ptr(), idx.data_ptr(), Tg.data_ptr(),
-                                                 st.data_ptr(), ws, wsb, self._lib.stream_handle()),
-                        "dr_shard_scan_deferred")
+        if self.deferred:
+            self._lib.check(L.dr_shard_scan_deferred(w.data_ptr(), m, V.data_ptr(), idx.data_ptr(), Tg.data_ptr(),
+                                                     st.data_ptr(), ws, wsb, self._lib.stream_handle()),
+                            "dr_shard_scan_deferred")
+        else:
+            self._lib.check(L.dr_shard_scan(w.data_ptr(), m, V.data_ptr(), Tg.data_ptr(), st.data_ptr(), ws, wsb,
+                                            self._lib.stream_handle()), "dr_shard_scan")
         return _ShardScan(V, idx), Tg, st
 
     def finalize(self, S, totals: torch.Tensor, G: int, g: int):
         """(values, index) of the shard once the totals are known: the header
-        {T, 2, O_g, pin} and the index levels of W (dr_shard_finalize_deferred)."""
+        {T, 2, O_g, pin} and the index levels of W (dr_shard_finalize_deferred),
+        or W = min((O_g + S) / T, 1) in place and its index (dr_shard_finalize)."""
         if S.numel() == 0:
             return S.V, None
-        self._lib.check(self._lib.lib().dr_shard_finalize_deferred(S.numel(), totals.data_ptr(), G, g,
-                                                                   S.idx.data_ptr(), self._lib.stream_handle()),
-                        "dr_shard_finalize_deferred")
+        L = self._lib.lib()
+        if self.deferred:
+            self._lib.check(L.dr_shard_finalize_deferred(S.numel(), totals.data_ptr(), G, g, S.idx.data_ptr(),
+                                                         self._lib.stream_handle()), "dr_shard_finalize_deferred")
+        else:
+            self._lib.check(L.dr_shard_finalize(S.V.data_ptr(), S.numel(), totals.data_ptr(), G, g,
+                                                S.idx.data_ptr(), self._lib.stream_handle()), "dr_shard_finalize")
         return S.V, S.idx
 
     def materialize(self, V: torch.Tensor, idx: torch.Tensor | None) -> torch.Tensor:
@@ -210,16 +221,19 @@ def slice_capacity(table: ShardedWeightTable, n: int, tile: int, g: int | None =
     return min(n + 1, ocap + 3 * tile + 1), ocap
 
 
-def build_sharded_table(raw_shard, *, group=None, ops=None) -> ShardedWeightTable:
+def build_sharded_table(raw_shard, *, group=None, ops=None, deferred: bool = True) -> ShardedWeightTable:
     """Build this rank's shard of one weight table (collective over ``group``).
 
     ``raw_shard``: this rank's contiguous slice of the raw weights, in rank
-    order (it may be empty).  Raises the reference's ValueError on every rank
+    order (it may be empty).  ``deferred``: single-pass shards (the default;
+    16 bytes per entry and no pass over the shard after the all-gather) or
+    two-pass shards holding W (a table built once and sampled many times).
+    Raises the reference's ValueError on every rank
     when any shard is invalid, when the whole table is empty, or when the
     total is degenerate / overflowing -- always after the collective, so no
     rank is left waiting in it.
     """
-    ops = ops or DeviceShardOps()
+    ops = ops or DeviceShardOps(deferred)
     G = dist.get_world_size(group)
     g = dist.get_rank(group)
     w = raw_shard if isinstance(raw_shard, torch.Tensor) else torch.as_tensor(raw_shard, dtype=torch.float64)

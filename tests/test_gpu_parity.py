@@ -434,7 +434,7 @@ def test_batched_invalid_weights_raise(drs):
         drs.resample_batched(w, 8, [drs.RngStream(1, (b,)) for b in range(10)])
 
 
-def _shard_emulation(orc, w, N, key, off, Gs):
+def _shard_emulation(orc, w, N, key, off, Gs, deferred=True):
     """The shard steps for G ranks run one after another on one GPU, with the
     all-gathers replaced by concatenation: the sharded table == the oracle's,
     every rank's U window == dr_sorted_uniforms bit for bit although each rank
@@ -442,7 +442,7 @@ def _shard_emulation(orc, w, N, key, off, Gs):
     the indices == the oracle's DaC on the whole table."""
     from paper_2604_01356_b200.sharded import DeviceShardOps, ShardedWeightTable, slice_capacity
 
-    ops = DeviceShardOps()
+    ops = DeviceShardOps(deferred)
     M = w.size
     k0, k1 = key
     Uo, st_o = orc.sorted_uniforms(k0, k1, off, N)
@@ -486,13 +486,14 @@ def _shard_emulation(orc, w, N, key, off, Gs):
     return st_o
 
 
-def test_sharded_single_gpu_emulation(drs, orc):
+@pytest.mark.parametrize("deferred", [True, False])
+def test_sharded_single_gpu_emulation(drs, orc, deferred):
     rng = np.random.default_rng(1005)
     M, N = 1 << 20, (1 << 17) + 3
     w = np.exp(2 * rng.standard_normal(M))
     off = rng.integers(0, M - 1024)
     w[off:off + 1024] = (w.sum() - w[off:off + 1024].sum()) / 3 / 1024
-    _shard_emulation(orc, w, N, orc.key_of(2005), 0, (1, 2, 4, 8))
+    _shard_emulation(orc, w, N, orc.key_of(2005), 0, (1, 2, 4, 8), deferred)
 
 
 def test_sharded_repair_at_rank_boundary(drs, orc):
