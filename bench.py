@@ -424,6 +424,12 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
                        "timed": "the C ABI on preallocated table buffers (CUDA events, L2 flushed)",
                        "api_ms": tb_api,
                        "api_note": "build_weight_table(w_dev): the public call, allocating the table"}
+        tk = ROOT / "profiles" / f"traffic_k1_{cfg}.json"
+        if tk.exists():  # the single pass's DRAM bytes from a committed ncu capture
+            kt = json.loads(tk.read_text())
+            table_build["single_pass_kernel"] = {"traffic": kt.get("bytes_per_launch"),
+                                                 "duration_us_ncu": kt.get("duration_us_ncu"),
+                                                 "source": kt.get("source")}
 
     # ---- the particle filter's resampling step (the paper's loop: new weights every
     # step): build_weight_table + the benchmarked sampler, device-resident weights in

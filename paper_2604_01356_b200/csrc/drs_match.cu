@@ -444,26 +444,38 @@ int launch_merge(const double* W, const double* idx, int64_t M, const double* U,
   return launch_rc();
 }
 
-// the top guide (drs_common.cuh) from the finished level kt: one thread per
-// bucket, a bisection among level kt's entries (L2-resident, <= 16384 of them);
-// the storage tail past bucket B + 1 is zeroed
+// the top guide (drs_common.cuh) from the finished level kt: level kt
+// (<= 16384 entries, L2-resident) staged in shared memory by one TMA bulk copy
+// per CTA, then one thread per bucket bisects it there (a 14-step chain of
+// shared-memory reads instead of L2 round trips); the storage tail past
+// bucket B + 1 is zeroed
 __global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ idx, IndexDesc d) {
+  extern __shared__ __align__(128) double sL[];
+  __shared__ __align__(8) uint64_t bar;
   pdl_wait();
   pdl_trigger();
+  const int64_t nk = d.n[d.kt];
+  const uint32_t bytes = (uint32_t)(cdiv(nk, FANOUT) * FANOUT * 8);  // the level is padded to whole nodes
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_expect_tx(&bar, bytes);
+    bulk_g2s(sL, idx + d.off[d.kt], bytes, &bar);
+  }
+  __syncthreads();
   int32_t* G = reinterpret_cast<int32_t*>(idx + d.toff);
   const int64_t cap = 2 * tg_doubles(d), nb = ((int64_t)1 << d.tshift) + 2;
   const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  mbar_wait(&bar, 0);
   if (b >= cap) return;
   if (b >= nb) {
     G[b] = 0;
     return;
   }
   const double x = (double)b / (double)((int64_t)1 << d.tshift);  // exact
-  const double* L = idx + d.off[d.kt];
-  int64_t lo = 0, hi = d.n[d.kt] - 1;
+  int lo = 0, hi = (int)nk - 1;
   while (lo < hi) {
-    const int64_t m = (lo + hi) >> 1;
-    if (L[m] < x) lo = m + 1;
+    const int m = (lo + hi) >> 1;
+    if (sL[m] < x) lo = m + 1;
     else hi = m;
   }
   G[b] = (int32_t)lo;
@@ -472,7 +484,10 @@ __global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ id
 int launch_top_guide(int64_t M, double* idx, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
   if (!d.kt) return DRS_OK;
-  launch_pdl(k_build_top_guide, dim3((unsigned)cdiv(2 * tg_doubles(d), 256)), dim3(256), 0, st, idx, d);
+  static SmemLimit lim;
+  const size_t smem = (size_t)cdiv(d.n[d.kt], FANOUT) * FANOUT * 8;
+  lim.raise((const void*)k_build_top_guide, (size_t)(DRS_TG_ENTRIES + FANOUT) * 8);
+  launch_pdl(k_build_top_guide, dim3((unsigned)cdiv(2 * tg_doubles(d), 256)), dim3(256), smem, st, idx, d);
   return launch_rc();
 }
 

@@ -529,30 +529,42 @@ __global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, Sca
     if (p < cdiv(d.n[k], FANOUT) * FANOUT) idx[d.off[k] + p] = dinf();
   }
   const DivBy byT = div_by(T);
-  const int64_t n1 = d.n[1];  // level 1 starts at offset 0 (16-byte aligned)
+  // level-1 entry m ends W block m (position 16 m + 15, the last one M - 1),
+  // which lies in table tile m / 528 (TABLE_TILE = 528 blocks); a pair
+  // (m, m + 1), m even, never straddles two tiles (528 is even)
+  static_assert(TABLE_TILE % (2 * FANOUT) == 0, "pairs of level-1 entries share a table tile");
+  constexpr uint32_t BLOCKS_PER_TILE = (uint32_t)(TABLE_TILE / FANOUT);
+  const int64_t n1 = d.n[1];  // level 1 starts at offset 0 (16-byte aligned); n1 < 2^32
   for (int64_t e = 2 * e0; e < n1; e += 2 * stride) {
     const bool two = e + 1 < n1;
     double2 l;
     if (two) l = *reinterpret_cast<const double2*>(idx + e);
     else l = make_double2(idx[e], 0.0);
+    const uint32_t tt = (uint32_t)e / BLOCKS_PER_TILE;
+    const double2 cd = FROM_WS ? make_double2(ws.grp[tt / GROUP_TILES], ws.incl[tt]) : __ldg(P + tt);
     double v[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t m = e + h;
-      const int64_t p = (m * FANOUT + FANOUT - 1 < M - 1) ? m * FANOUT + FANOUT - 1 : M - 1;
-      const int64_t tt = p / TABLE_TILE;
-      const double2 cd = FROM_WS ? make_double2(ws.grp[tt / GROUP_TILES], ws.incl[tt]) : __ldg(P + tt);
       const double sl = __dadd_rn(cd.x, __dadd_rn(cd.y, h ? l.y : l.x));
       const double S = shard ? __dadd_rn(O, sl) : sl;
-      v[h] = (p == M - 1 && pin) ? 1.0 : fmin(div_rn(S, byT), 1.0);
-      if (m >= n1) continue;
-      for (int k = 2, sh = 8; k <= d.levels; ++k, sh += 4) {
-        if (p != M - 1 && ((p + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
-        idx[d.off[k] + (p >> sh)] = v[h];
-      }
+      const bool last = e + h == n1 - 1;  // block n1 - 1 ends at M - 1
+      v[h] = (last && pin) ? 1.0 : fmin(div_rn(S, byT), 1.0);
     }
     if (two) *reinterpret_cast<double2*>(idx + e) = make_double2(v[0], v[1]);
     else idx[e] = v[0];
+    // the higher levels: entry m ends a level-k block when (m + 1) is a
+    // multiple of 16^(k-1) (only an odd m can), or m is the last entry
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t m = e + h;
+      if (h == 1 && !two) break;
+      const bool lastm = m == n1 - 1;
+      if (!lastm && ((m + 1) & (FANOUT - 1)) != 0) continue;
+      for (int k = 2, sh = 4; k <= d.levels; ++k, sh += 4) {
+        if (!lastm && ((m + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
+        idx[d.off[k] + (m >> sh)] = v[h];
+      }
+    }
   }
 }
 
@@ -801,7 +813,8 @@ static int build_deferred(const double* w, bool logw, int64_t M, double* L, doub
   launch_chain(s, nt, 0, status, nullptr, st);
   int64_t work = nt;
   if (d.levels > 0) work = std::max<int64_t>(work, std::max<int64_t>(cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels));
-  const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * 8);
+  static OccupancyCache occ_l;
+  const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * occ_l.get((const void*)k_table_levels<true>, 256, 0));
   launch_pdl(k_table_levels<true>, dim3((unsigned)lgrid), dim3(256), 0, st, M, nt, s, idx, d);
   if (launch_rc()) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
@@ -849,7 +862,8 @@ int launch_table_levels_from_aux(int64_t M, double* idx, cudaStream_t st) {
   const ScanWS none{};
   int64_t work = 1;
   if (d.levels > 0) work = std::max<int64_t>(cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels);
-  const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * 8);
+  static OccupancyCache occ_l;
+  const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * occ_l.get((const void*)k_table_levels<false>, 256, 0));
   launch_pdl(k_table_levels<false>, dim3((unsigned)lgrid), dim3(256), 0, st, M, (int64_t)0, none, idx, d);
   if (launch_rc()) return DRS_ERR_LAUNCH;
   return launch_top_guide(M, idx, st);
