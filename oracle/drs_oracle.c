@@ -237,6 +237,24 @@ int drs_ref_build_table(const double *w, int64_t M, double *W) {
   return st;
 }
 
+/* A deferred table whose top guide sits above level 1 (kt >= 2) keeps its
+ * level-1 index entries as in-tile values: level 1 (offset 0) gets V at the
+ * 16-entry block ends.  Returns 1 when it did (the header's mode bit 4). */
+static void ref_top_guide(int64_t M, int *kt, int64_t *nkt, int *tshift, int64_t *tdoubles);
+int drs_ref_index_l1_local(const double *V, int64_t M, double *idx) {
+  int kt, tshift;
+  int64_t nkt, td;
+  ref_top_guide(M, &kt, &nkt, &tshift, &td);
+  if (kt < 2) return 0;
+  const int64_t n1 = (M + DRS_REF_FANOUT - 1) / DRS_REF_FANOUT;
+  for (int64_t m = 0; m < n1; ++m) {
+    int64_t p = m * DRS_REF_FANOUT + DRS_REF_FANOUT - 1;
+    if (p > M - 1) p = M - 1;
+    idx[m] = V[p];
+  }
+  return 1;
+}
+
 /* dr_build_table_deferred (the single-pass table): the same association as
  * drs_ref_chain_scan, split at the tile prefix: V[j] = R + (Q + s) (the
  * in-tile sums), per tile the pair {C_g, D_t}, so that S = C_g + (D_t + V[j]);
@@ -286,9 +304,10 @@ int drs_ref_build_table_deferred(const double *w, int64_t M, double *V, double *
   }
   W[M - 1] = 1.0;
   drs_ref_build_index(W, M, idx);
+  const int l1 = drs_ref_index_l1_local(V, M, idx);
   double *aux = idx + drs_ref_search_entries(M);
   aux[0] = T;
-  aux[1] = 1.0; /* mode 1: S = C + (D + V) */
+  aux[1] = l1 ? 5.0 : 1.0; /* mode 1: S = C + (D + V); + 4: level 1 holds V */
   aux[2] = 0.0; /* O (shards only) */
   aux[3] = 1.0; /* the last entry pinned to 1 */
   memcpy(aux + 4, P, sizeof(double) * 2 * (size_t)nt);

@@ -68,6 +68,7 @@ int drs_ref_sorted_uniforms_from(const double *raw, int64_t n, double *U);
 int64_t drs_ref_index_entries(int64_t M);
 int64_t drs_ref_search_entries(int64_t M);
 int drs_ref_build_table_deferred(const double *w, int64_t M, double *V, double *idx, double *Wout);
+int drs_ref_index_l1_local(const double *V, int64_t M, double *idx);
 void drs_ref_build_index(const double *W, int64_t M, double *idx);
 int drs_ref_build_table_sharded(const double *w, int64_t M, int G, double *W,
                                 double *shard_totals);

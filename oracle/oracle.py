@@ -38,6 +38,7 @@ _PROTOS = {
     "drs_ref_index_entries": (_I64, [_I64]),
     "drs_ref_search_entries": (_I64, [_I64]),
     "drs_ref_build_table_deferred": (_INT, [_P, _I64, _P, _P, _P]),
+    "drs_ref_index_l1_local": (_INT, [_P, _I64, _P]),
     "drs_ref_build_index": (None, [_P, _I64, _P]),
     "drs_ref_build_table_sharded": (_INT, [_P, _I64, _INT, _P, _P]),
     "drs_ref_resample_batched": (_INT, [_P, _I64, _I64, _I64, _P, _P, _P, _P]),
@@ -197,6 +198,16 @@ def build_table_deferred(w):
     idx = np.empty(int(lib().drs_ref_index_entries(w.size)), dtype=np.float64)
     st = lib().drs_ref_build_table_deferred(_p(w), w.size, _p(V), _p(idx), _p(W))
     return V, idx, W, int(st)
+
+
+def index_l1_local(V, idx):
+    """The index of a deferred table whose level 1 keeps in-tile values (top
+    guide above level 1): idx (a copy) with level 1 = V at the block ends;
+    (idx, True) when that applies, else (idx, False)."""
+    V = _f64(V)
+    idx = np.array(idx, dtype=np.float64, copy=True)
+    done = lib().drs_ref_index_l1_local(_p(V), V.size, _p(idx))
+    return idx, bool(done)
 
 
 def match(kind, W, u):

@@ -53,14 +53,15 @@ struct SmemLevels {
   int64_t base;     // idx offset of level k_smem
   int64_t count;    // doubles staged
   int tg;           // the top guide is staged too (k_smem == kt): the search enters at level kt
+  int64_t hdr;      // offset in the stage of the table header (it follows the guide), -1: not staged
 };
 
 SmemLevels plan_smem_levels(const IndexDesc& d, int64_t cap = SIDX_CAP) {
-  SmemLevels s{d.levels + 1, 0, 0, 0};
+  SmemLevels s{d.levels + 1, 0, 0, 0, -1};
   if (d.levels == 0) return s;
-  if (d.kt) {  // level kt, the levels above it and the top guide: one contiguous range
+  if (d.kt) {  // level kt, the levels above it, the top guide and the table header: one contiguous range
     const int64_t need = d.toff + tg_doubles(d) - d.off[d.kt];
-    if (need <= cap) return SmemLevels{d.kt, d.off[d.kt], need, 1};
+    if (need + TAB_HDR <= cap) return SmemLevels{d.kt, d.off[d.kt], need + TAB_HDR, 1, d.aoff - d.off[d.kt]};
   }
   const int64_t end = d.off[d.levels] + cdiv(d.n[d.levels], FANOUT) * FANOUT;
   for (int k = d.levels; k >= 1; --k) {
@@ -85,7 +86,8 @@ __device__ __forceinline__ int count_lt16_smem(const double* p, double x) {
 
 // K_UNIF independent searches in lock-step: the level loop is outside, so the
 // lines of a level are in flight together
-__device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const double* __restrict__ idx,
+template <bool DEF>
+__device__ __forceinline__ void search_k_sm_impl(const double* __restrict__ W, const double* __restrict__ idx,
                                             const double* sidx, const IndexDesc& d, const SmemLevels& sl,
                                             const TabAux& ta, const double x[K_UNIF], int64_t r[K_UNIF]) {
   int64_t b[K_UNIF];
@@ -112,12 +114,36 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
     }
     ktop = d.kt - 1;
   }
+  // a deferred table's tile pair and band of each u: formed at level 1 when
+  // that level holds in-tile values (TAB_L1: its 256-entry node and the W
+  // line below lie in one tile), else at the W line
+  double2 cd[K_UNIF];
+  WKey key[K_UNIF];
+  bool have = false;
   for (int k = ktop; k >= 1; --k) {
     int c[K_UNIF];
     if (k >= sl.k_smem) {
       const double* base = sidx + (d.off[k] - sl.base);
 #pragma unroll
       for (int q = 0; q < K_UNIF; ++q) c[q] = count_lt16_smem(base + FANOUT * b[q], x[q]);
+    } else if (DEF && k == 1 && ta.l1) {
+      const double* base = idx + d.off[1];
+      double v1[K_UNIF][16];
+#pragma unroll
+      for (int q = 0; q < K_UNIF; ++q) {
+        const double* p = base + FANOUT * b[q];
+        ldg256(p + 0, v1[q][0], v1[q][1], v1[q][2], v1[q][3]);
+        ldg256(p + 4, v1[q][4], v1[q][5], v1[q][6], v1[q][7]);
+        ldg256(p + 8, v1[q][8], v1[q][9], v1[q][10], v1[q][11]);
+        ldg256(p + 12, v1[q][12], v1[q][13], v1[q][14], v1[q][15]);
+        cd[q] = __ldg(ta.P + b[q] / (TABLE_TILE / (FANOUT * FANOUT)));
+      }
+#pragma unroll
+      for (int q = 0; q < K_UNIF; ++q) {
+        key[q] = tab_wkey(ta, x[q]);
+        c[q] = count_w16(v1[q], ta, cd[q], x[q], key[q]);
+      }
+      have = true;
     } else {
       const double* base = idx + d.off[k];
 #pragma unroll
@@ -134,7 +160,6 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
   // short tail line is re-read scalar), so the DRAM round trips overlap; a
   // deferred table's tile pairs and keys are formed while they are in flight
   double v[K_UNIF][16];
-  double2 cd[K_UNIF];
 #pragma unroll
   for (int q = 0; q < K_UNIF; ++q) {
     const int64_t j0 = FANOUT * b[q];
@@ -143,20 +168,39 @@ __device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const 
     ldg256(p + 4, v[q][4], v[q][5], v[q][6], v[q][7]);
     ldg256(p + 8, v[q][8], v[q][9], v[q][10], v[q][11]);
     ldg256(p + 12, v[q][12], v[q][13], v[q][14], v[q][15]);
-    cd[q] = ta.def ? __ldg(ta.P + j0 / TABLE_TILE) : make_double2(0.0, 0.0);
+    if (DEF && !have) cd[q] = __ldg(ta.P + j0 / TABLE_TILE);
   }
-  WKey key[K_UNIF];
+  if (DEF && !have) {
 #pragma unroll
-  for (int q = 0; q < K_UNIF; ++q) key[q] = tab_wkey(ta, x[q]);
+    for (int q = 0; q < K_UNIF; ++q) key[q] = tab_wkey(ta, x[q]);
+  }
 #pragma unroll
   for (int q = 0; q < K_UNIF; ++q) {
     const int64_t j0 = FANOUT * b[q];
     const int64_t valid = d.n[0] - j0;
-    int c = (valid >= FANOUT) ? count_w16(v[q], ta, cd[q], x[q], key[q])
-                              : count_w_tail(W, j0, (int)valid, ta, cd[q], x[q]);
+    int c = 0;
+    if (DEF) {
+      c = (valid >= FANOUT) ? count_w16(v[q], ta, cd[q], x[q], key[q])
+                            : count_w_tail(W, j0, (int)valid, ta, cd[q], x[q]);
+    } else if (valid >= FANOUT) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) c += (v[q][i] < x[q]) ? 1 : 0;
+    } else {
+      for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
+    }
     if (c >= valid) c = (int)valid - 1;
     r[q] = j0 + c;
   }
+}
+
+// one search body per kind of table (the header is uniform across the
+// grid): a direct table runs exactly the compare-W code, with no
+// deferred-table state live in it
+__device__ __forceinline__ void search_k_sm(const double* __restrict__ W, const double* __restrict__ idx,
+                                            const double* sidx, const IndexDesc& d, const SmemLevels& sl,
+                                            const TabAux& ta, const double x[K_UNIF], int64_t r[K_UNIF]) {
+  if (ta.def) search_k_sm_impl<true>(W, idx, sidx, d, sl, ta, x, r);
+  else search_k_sm_impl<false>(W, idx, sidx, d, sl, ta, x, r);
 }
 
 // The throughput variant for many u's (k_match_index_sm): KQ searches per
@@ -194,8 +238,8 @@ __device__ __forceinline__ int count_w16_half(const double* p, const TabAux& ta,
   return c;
 }
 
-template <int KQ>
-__device__ __forceinline__ void search_half(const double* __restrict__ W, const double* __restrict__ idx,
+template <int KQ, bool DEF>
+__device__ __forceinline__ void search_half_impl(const double* __restrict__ W, const double* __restrict__ idx,
                                             const double* sidx, const IndexDesc& d, const SmemLevels& sl,
                                             const TabAux& ta, const double x[KQ], int64_t r[KQ]) {
   int64_t b[KQ];
@@ -220,12 +264,25 @@ __device__ __forceinline__ void search_half(const double* __restrict__ W, const 
     }
     ktop = d.kt - 1;
   }
+  double2 cd[KQ];
+  WKey key[KQ];
+  bool have = false;
   for (int k = ktop; k >= 1; --k) {
     int c[KQ];
     if (k >= sl.k_smem) {
       const double* base = sidx + (d.off[k] - sl.base);
 #pragma unroll
       for (int q = 0; q < KQ; ++q) c[q] = count_lt16_smem(base + FANOUT * b[q], x[q]);
+    } else if (DEF && k == 1 && ta.l1) {  // level 1 in-tile (its node and the W line share a tile)
+      const double* base = idx + d.off[1];
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) {
+        cd[q] = __ldg(ta.P + b[q] / (TABLE_TILE / (FANOUT * FANOUT)));
+        key[q] = tab_wkey(ta, x[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < KQ; ++q) c[q] = count_w16_half(base + FANOUT * b[q], ta, cd[q], x[q], key[q]);
+      have = true;
     } else {
       const double* base = idx + d.off[k];  // levels are padded to whole nodes with +inf
 #pragma unroll
@@ -238,22 +295,37 @@ __device__ __forceinline__ void search_half(const double* __restrict__ W, const 
       b[q] = FANOUT * b[q] + c[q];
     }
   }
-  double2 cd[KQ];
-  WKey key[KQ];
+  if (DEF && !have) {
 #pragma unroll
-  for (int q = 0; q < KQ; ++q) {
-    cd[q] = ta.def ? __ldg(ta.P + FANOUT * b[q] / TABLE_TILE) : make_double2(0.0, 0.0);
-    key[q] = tab_wkey(ta, x[q]);
+    for (int q = 0; q < KQ; ++q) {
+      cd[q] = __ldg(ta.P + FANOUT * b[q] / TABLE_TILE);
+      key[q] = tab_wkey(ta, x[q]);
+    }
   }
 #pragma unroll
   for (int q = 0; q < KQ; ++q) {
     const int64_t j0 = FANOUT * b[q];
     const int64_t valid = d.n[0] - j0;
-    int c = (valid >= FANOUT) ? count_w16_half(W + j0, ta, cd[q], x[q], key[q])
-                              : count_w_tail(W, j0, (int)valid, ta, cd[q], x[q]);
+    int c = 0;
+    if (DEF) {
+      c = (valid >= FANOUT) ? count_w16_half(W + j0, ta, cd[q], x[q], key[q])
+                            : count_w_tail(W, j0, (int)valid, ta, cd[q], x[q]);
+    } else if (valid >= FANOUT) {
+      c = count_lt16_half(W + j0, x[q]);
+    } else {
+      for (int i = 0; i < (int)valid; ++i) c += (__ldg(W + j0 + i) < x[q]) ? 1 : 0;
+    }
     if (c >= valid) c = (int)valid - 1;
     r[q] = j0 + c;
   }
+}
+
+template <int KQ>
+__device__ __forceinline__ void search_half(const double* __restrict__ W, const double* __restrict__ idx,
+                                            const double* sidx, const IndexDesc& d, const SmemLevels& sl,
+                                            const TabAux& ta, const double x[KQ], int64_t r[KQ]) {
+  if (ta.def) search_half_impl<KQ, true>(W, idx, sidx, d, sl, ta, x, r);
+  else search_half_impl<KQ, false>(W, idx, sidx, d, sl, ta, x, r);
 }
 
 // Sense-free grid barrier for a cooperative launch (all CTAs co-resident).
@@ -333,16 +405,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
     const int64_t p0 = plo + t * per, p1 = min(a.sl.base, p0 + per) & ~(int64_t)1;
     for (int64_t p = p0 & ~(int64_t)1; p < p1; p += 8192)  // 64 KB pieces
       prefetch_l2(a.idx + p, (uint32_t)(min((int64_t)8192, p1 - p) * 8));
-    // the table's tile pairs (a deferred table's W line needs its tile's
-    // pair: 16 bytes per 8448 entries, 127 KB at M = 2^26), one slice per CTA
-    const int64_t pb = a.d.aoff + TAB_HDR, pn = 2 * table_tiles(a.d.n[0]);
-    const int64_t pper = cdiv(cdiv(pn, (int64_t)gridDim.x), 2) * 2;
-    const int64_t q0 = t * pper, q1 = min(pn, q0 + pper);
-    for (int64_t q = q0; a.idx && q < q1; q += 8192)
-      prefetch_l2(a.idx + pb + q, (uint32_t)(min((int64_t)8192, q1 - q) * 8));
   }
   const unsigned long long gen = *(volatile unsigned long long*)&a.ws.hdr->fgen;
-  const TabAux ta = load_aux(a.idx ? a.idx + a.d.aoff : nullptr);  // consumed by the search
   const uint64_t offset = a.offset_dev ? *(volatile uint64_t*)a.offset_dev : a.offset;
   __syncthreads();
   STAMP(0);
@@ -388,6 +452,20 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   }
   __syncthreads();
   STAMP(9);
+  if (threadIdx.x == THREADS - 32 && a.sl.hdr >= 0) {
+    // a deferred table's tile pairs (a W line, or a level-1 node, needs its
+    // tile's pair: 16 bytes per 8448 entries, 127 KB at M = 2^26) into L2, one
+    // slice per CTA, while warp 0 folds the chain; the header came with the staged
+    // levels (which have landed by now), so a direct table skips this
+    mbar_wait(&bar, 0);
+    if (sidx[a.sl.hdr + 1] != 0.0) {
+      const int64_t pb = a.d.aoff + TAB_HDR, pn = 2 * table_tiles(a.d.n[0]);
+      const int64_t pper = cdiv(cdiv(pn, (int64_t)gridDim.x), 2) * 2;
+      const int64_t q0 = t * pper, q1 = min(pn, q0 + pper);
+      for (int64_t q = q0; q < q1; q += 8192)
+        prefetch_l2(a.idx + pb + q, (uint32_t)(min((int64_t)8192, q1 - q) * 8));
+    }
+  }
   if (warp == 0) {
     // the nt totals and minima arrive by coalesced L2 loads (.cg: no stale
     // L1 copies of the previous call's values) into shared memory, padded
@@ -503,6 +581,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   STAMP(5);
   mbar_wait(&bar, 0);
   STAMP(6);
+  // the table header arrived with the staged levels (no global round trip here)
+  const TabAux ta = (a.sl.hdr >= 0) ? tab_aux_at(sidx + a.sl.hdr, a.idx + a.d.aoff)
+                                    : load_aux(a.idx ? a.idx + a.d.aoff : nullptr);
   int64_t r[K_UNIF];
   search_k_sm(a.W, a.idx, sidx, a.d, a.sl, ta, u, r);
   STAMP(7);
@@ -586,7 +667,7 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t off = offset_dev ? *(volatile uint64_t*)offset_dev : offset;
-  const TabAux ta = load_aux(idx ? idx + d.aoff : nullptr);
+  TabAux ta;
   bool staged = false;
   static_assert(K_UNIF == 2, "two draws per thread per chunk");
   for (int64_t base = (int64_t)blockIdx.x * 2 * blockDim.x; base < N; base += (int64_t)gridDim.x * 2 * blockDim.x) {
@@ -601,6 +682,7 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
     if (!staged) {
       mbar_wait(&bar, 0);
       staged = true;
+      ta = (sl.hdr >= 0) ? tab_aux_at(sidx + sl.hdr, idx + d.aoff) : load_aux(idx ? idx + d.aoff : nullptr);
     }
     int64_t r[K_UNIF];
     search_k_sm(W, idx, sidx, d, sl, ta, u, r);
@@ -619,21 +701,33 @@ __global__ void __launch_bounds__(256) k_sample_binary_sm(const double* __restri
 #ifndef MATCH_KQ
 #define MATCH_KQ 4  // u's per thread in lock-step
 #endif
+#ifndef MATCH_KQ_DEF
+#define MATCH_KQ_DEF 2  // the same on a deferred table (its band per u: registers)
+#endif
 // rng (optional, on the device, the range8 of include/drs.h): search only
 // global u's rng[0] .. rng[1] of the windows u (base rng[4]) and out (base
 // rng[5]) and add `shift` to the indices (a W shard of a sharded table)
-// THROUGHPUT: MATCH_KQ searches per thread reading half nodes (search_half),
-// for many u's per CTA; else two full-node searches per thread (search_k_sm),
-// the latency-bound case of few u's
-template <bool THROUGHPUT>
+// KIND 0: two full-node searches per thread (search_k_sm), the latency-bound
+// case of few u's, either kind of table; KIND 1 / 2: MATCH_KQ searches per
+// thread reading half nodes (search_half), for many u's per CTA, on a direct /
+// a deferred table only -- the two are launched together and the one that
+// does not match the table's header exits at once, so each compiles for its
+// own kind (the deferred search's state would otherwise cost the direct one
+// half its resident CTAs: 128 registers against 52)
+template <int KIND>
 __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict__ W, const double* __restrict__ idx,
                                                         IndexDesc d, SmemLevels sl, const double* __restrict__ u,
                                                         int64_t N, int64_t* __restrict__ out,
                                                         const int64_t* __restrict__ rng, int64_t shift) {
+  constexpr bool THROUGHPUT = KIND != 0;
   extern __shared__ __align__(128) double sidx[];
   __shared__ __align__(8) uint64_t bar;
   const uint32_t sbytes = (uint32_t)(sl.count * 8);
   pdl_wait();
+  if (THROUGHPUT) {
+    const bool def = idx && __ldg(idx + d.aoff + 1) != 0.0;
+    if (def != (KIND == 2)) return;
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, sbytes);
@@ -642,13 +736,13 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
   __syncthreads();
   pdl_trigger();
   mbar_wait(&bar, 0);
-  const TabAux ta = load_aux(idx ? idx + d.aoff : nullptr);
+  const TabAux ta = (sl.hdr >= 0) ? tab_aux_at(sidx + sl.hdr, idx + d.aoff) : load_aux(idx ? idx + d.aoff : nullptr);
   const int64_t lo = rng ? rng[0] : 0, hi = rng ? rng[1] : N;
   if (rng) {  // sharded: U and out are windows with global bases rng[4], rng[5]
     u -= rng[4];
     out -= rng[5];
   }
-  constexpr int KQ = THROUGHPUT ? MATCH_KQ : K_UNIF;
+  constexpr int KQ = KIND == 1 ? MATCH_KQ : (KIND == 2 ? MATCH_KQ_DEF : K_UNIF);
   for (int64_t base = lo + (int64_t)blockIdx.x * KQ * blockDim.x; base < hi;
        base += (int64_t)gridDim.x * KQ * blockDim.x) {
     double x[KQ];
@@ -659,7 +753,8 @@ __global__ void __launch_bounds__(256) k_match_index_sm(const double* __restrict
       x[h] = (i[h] < hi) ? __ldg(u + i[h]) : 0.5;
     }
     int64_t r[KQ];
-    if constexpr (THROUGHPUT) search_half<KQ>(W, idx, sidx, d, sl, ta, x, r);
+    if constexpr (KIND == 1) search_half_impl<KQ, false>(W, idx, sidx, d, sl, ta, x, r);
+    else if constexpr (KIND == 2) search_half_impl<KQ, true>(W, idx, sidx, d, sl, ta, x, r);
     else search_k_sm(W, idx, sidx, d, sl, ta, x, r);
 #pragma unroll
     for (int h = 0; h < KQ; ++h)
@@ -671,25 +766,30 @@ int launch_index_sm(const double* W, const double* idx, int64_t M, const double*
                     cudaStream_t st, const int64_t* rng, int64_t shift) {
   const IndexDesc d = make_index_desc(M);
   const SmemLevels sl = plan_smem_levels(d, DRS_MATCH_SMEM_CAP);
-  static SmemLimit lim, lim_t;
-  static OccupancyCache occ, occ_t;
+  static SmemLimit lim, lim_1, lim_2;
+  static OccupancyCache occ, occ_1, occ_2;
   const size_t smem = (size_t)sl.count * 8;
-  lim.raise((const void*)k_match_index_sm<false>, SIDX_CAP * 8);
-  lim_t.raise((const void*)k_match_index_sm<true>, SIDX_CAP * 8);
-  const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_match_index_sm<false>, 256, smem);
+  lim.raise((const void*)k_match_index_sm<0>, SIDX_CAP * 8);
+  lim_1.raise((const void*)k_match_index_sm<1>, SIDX_CAP * 8);
+  lim_2.raise((const void*)k_match_index_sm<2>, SIDX_CAP * 8);
+  const int64_t cap = (int64_t)drs_sm_count() * occ.get((const void*)k_match_index_sm<0>, 256, smem);
   // many u's per resident CTA: the data pipe bounds the searches (half nodes,
   // MATCH_KQ per thread); few: the dependent round trips do (full nodes, two)
   if (cdiv(N, 256 * K_UNIF) >= 4 * cap) {
-    const int64_t cap_t = (int64_t)drs_sm_count() * occ_t.get((const void*)k_match_index_sm<true>, 256, smem);
     const int64_t chunks = cdiv(N, 256 * MATCH_KQ);
-    const int64_t grid = chunks < cap_t ? chunks : cap_t;
-    launch_pdl(k_match_index_sm<true>, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng,
-               shift);
+    const int64_t cap_1 = (int64_t)drs_sm_count() * occ_1.get((const void*)k_match_index_sm<1>, 256, smem);
+    const int64_t cap_2 = (int64_t)drs_sm_count() * occ_2.get((const void*)k_match_index_sm<2>, 256, smem);
+    // one of the two exits at its first instruction (the table header)
+    launch_pdl(k_match_index_sm<1>, dim3((unsigned)(chunks < cap_1 ? chunks : cap_1)), dim3(256), smem, st, W, idx,
+               d, sl, u, N, out, rng, shift);
+    const int64_t chunks_2 = cdiv(N, 256 * MATCH_KQ_DEF);
+    launch_pdl(k_match_index_sm<2>, dim3((unsigned)(chunks_2 < cap_2 ? chunks_2 : cap_2)), dim3(256), smem, st, W, idx,
+               d, sl, u, N, out, rng, shift);
     return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
   }
   const int64_t chunks = cdiv(N, 256 * K_UNIF);
   const int64_t grid = chunks < cap ? chunks : cap;
-  launch_pdl(k_match_index_sm<false>, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
+  launch_pdl(k_match_index_sm<0>, dim3((unsigned)grid), dim3(256), smem, st, W, idx, d, sl, u, N, out, rng, shift);
   return cudaGetLastError() == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 

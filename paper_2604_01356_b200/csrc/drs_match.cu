@@ -130,11 +130,18 @@ __device__ __forceinline__ void stage_to_w(double* sw, int len, int64_t j0, int6
 }
 
 // W[j] at the end of a 16-entry block (j = 16 m + 15, or M - 1): level 1 of
-// the index holds exactly these values for either kind of table (W itself,
-// never a deferred table's in-tile value); a table without an index is direct
+// the index holds these values -- W itself, or (TAB_L1) the in-tile value,
+// turned into W with the header and the tile pair (loaded after the header:
+// only such tables pay the second round trip); a table without an index is
+// direct
 __device__ __forceinline__ double block_end_w(const double* __restrict__ W, const double* __restrict__ idx,
-                                              int64_t M, int64_t j) {
-  return (idx && M > FANOUT) ? __ldg(idx + j / FANOUT) : __ldg(W + j);  // level 1 sits at offset 0
+                                              const double* __restrict__ aux, int64_t M, int64_t j) {
+  if (!(idx && M > FANOUT)) return __ldg(W + j);
+  const double v = __ldg(idx + j / FANOUT);  // level 1 sits at offset 0
+  const double2 h = __ldg(reinterpret_cast<const double2*>(aux));
+  if (!((int)h.y & TAB_L1)) return v;
+  const TabAux ta = load_aux(aux);
+  return tab_w(ta, __ldg(ta.P + j / TABLE_TILE), v, j == M - 1);
 }
 
 constexpr int MT_THREADS = 256;
@@ -184,10 +191,10 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
     s_probe = 0;
   }
   if (warp == 0) {  // tile edges are block ends (tw is a multiple of 16): level 1 holds W there
-    const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, block_end_w(W, idx, M, j0 - 1));
+    const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, block_end_w(W, idx, aux, M, j0 - 1));
     if (lane == 0) s_ib = v;
   } else if (warp == 1) {
-    const int64_t v = last ? N : warp_count_le(U, N, block_end_w(W, idx, M, j0 + len - 1));
+    const int64_t v = last ? N : warp_count_le(U, N, block_end_w(W, idx, aux, M, j0 + len - 1));
     if (lane == 0) s_ie = v;
   }
   __syncthreads();
@@ -223,7 +230,7 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
             const int mid = (lo + hi) >> 1;
             const double2 cd = s_pair[mid < jb ? 0 : 1];
             double S = __dadd_rn(cd.x, __dadd_rn(cd.y, sw[mid]));
-            if (s_hdr.y == 2.0) S = __dadd_rn(s_hdr2.x, S);  // a shard of a W-sharded table
+            if ((int)s_hdr.y & TAB_SHARD) S = __dadd_rn(s_hdr2.x, S);  // a shard of a W-sharded table
             const double v = (j0 + mid == M - 1 && s_hdr2.y != 0.0) ? 1.0 : fmin(__ddiv_rn(S, s_hdr.x), 1.0);
             if (v < x) lo = mid + 1;
             else hi = mid;

@@ -505,13 +505,14 @@ __global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, Sca
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   double T, O = 0.0;
   bool shard = false, pin = true;
+  const bool l1 = d.kt >= 2;  // level 1 keeps its in-tile values (TAB_L1)
   if (FROM_WS) {
     T = ws.hdr->total;
     for (int64_t e = e0; e < nt; e += stride)
       reinterpret_cast<double2*>(aux + TAB_HDR)[e] = make_double2(ws.grp[e / GROUP_TILES], ws.incl[e]);
     if (e0 == 0) {
       aux[0] = T;
-      aux[1] = 1.0;
+      aux[1] = (double)(TAB_DEFERRED | (l1 ? TAB_L1 : 0));
       aux[2] = 0.0;
       aux[3] = 1.0;
     }
@@ -535,6 +536,25 @@ __global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, Sca
   static_assert(TABLE_TILE % (2 * FANOUT) == 0, "pairs of level-1 entries share a table tile");
   constexpr uint32_t BLOCKS_PER_TILE = (uint32_t)(TABLE_TILE / FANOUT);
   const int64_t n1 = d.n[1];  // level 1 starts at offset 0 (16-byte aligned); n1 < 2^32
+  if (l1) {
+    // level 1 stays in-tile: only the entries of level 2 and above, each the
+    // W of its level-1 source entry m = 16 m2 + 15 (the last: n1 - 1)
+    for (int64_t m2 = e0; m2 < d.n[2]; m2 += stride) {
+      const int64_t m = (m2 * FANOUT + FANOUT - 1 < n1 - 1) ? m2 * FANOUT + FANOUT - 1 : n1 - 1;
+      const uint32_t tt = (uint32_t)m / BLOCKS_PER_TILE;
+      const double2 cd = FROM_WS ? make_double2(ws.grp[tt / GROUP_TILES], ws.incl[tt]) : __ldg(P + tt);
+      const double sl = __dadd_rn(cd.x, __dadd_rn(cd.y, idx[m]));
+      const double S = shard ? __dadd_rn(O, sl) : sl;
+      const bool lastm = m == n1 - 1;
+      const double v = (lastm && pin) ? 1.0 : fmin(div_rn(S, byT), 1.0);
+      idx[d.off[2] + m2] = v;
+      for (int k = 3, sh = 8; k <= d.levels; ++k, sh += 4) {
+        if (!lastm && ((m + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
+        idx[d.off[k] + (m >> sh)] = v;
+      }
+    }
+    return;
+  }
   for (int64_t e = 2 * e0; e < n1; e += 2 * stride) {
     const bool two = e + 1 < n1;
     double2 l;
@@ -812,7 +832,8 @@ static int build_deferred(const double* w, bool logw, int64_t M, double* L, doub
   }
   launch_chain(s, nt, 0, status, nullptr, st);
   int64_t work = nt;
-  if (d.levels > 0) work = std::max<int64_t>(work, std::max<int64_t>(cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels));
+  if (d.levels > 0)
+    work = std::max<int64_t>(work, std::max<int64_t>(d.kt >= 2 ? d.n[2] : cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels));
   static OccupancyCache occ_l;
   const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * occ_l.get((const void*)k_table_levels<true>, 256, 0));
   launch_pdl(k_table_levels<true>, dim3((unsigned)lgrid), dim3(256), 0, st, M, nt, s, idx, d);
@@ -861,7 +882,7 @@ int launch_table_levels_from_aux(int64_t M, double* idx, cudaStream_t st) {
   const IndexDesc d = make_index_desc(M);
   const ScanWS none{};
   int64_t work = 1;
-  if (d.levels > 0) work = std::max<int64_t>(cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels);
+  if (d.levels > 0) work = std::max<int64_t>(d.kt >= 2 ? d.n[2] : cdiv(d.n[1], 2), (int64_t)FANOUT * d.levels);
   static OccupancyCache occ_l;
   const int64_t lgrid = std::min<int64_t>(cdiv(work, 256), (int64_t)drs_sm_count() * occ_l.get((const void*)k_table_levels<false>, 256, 0));
   launch_pdl(k_table_levels<false>, dim3((unsigned)lgrid), dim3(256), 0, st, M, (int64_t)0, none, idx, d);

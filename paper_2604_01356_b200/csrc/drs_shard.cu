@@ -45,13 +45,13 @@ __global__ void k_shard_finalize(double* __restrict__ S, int64_t Mg, const doubl
   }
 }
 
-// the header of a deferred shard {T, 2, O_g, pin}: S = O_g + (C + (D + L)),
+// the header of a deferred shard {T, mode 1|2 (+4), O_g, pin}: S = O_g + (C + (D + L)),
 // W = min(S / T, 1), only the last shard's last entry pinned to 1
-__global__ void k_shard_header(const double* __restrict__ totals, int G, int g, double* __restrict__ aux) {
+__global__ void k_shard_header(const double* __restrict__ totals, int G, int g, double* __restrict__ aux, int l1) {
   double Og, Og1, T;
   fold_offsets(totals, G, g, Og, Og1, T);
   aux[0] = T;
-  aux[1] = 2.0;
+  aux[1] = (double)(TAB_DEFERRED | TAB_SHARD | (l1 ? TAB_L1 : 0));
   aux[2] = Og;
   aux[3] = (g == G - 1) ? 1.0 : 0.0;
 }
@@ -328,7 +328,8 @@ int dr_shard_finalize_deferred(int64_t Mg, const double* totals, int32_t G, int3
                                void* stream) {
   if (Mg < 1 || !totals || !idx || G < 1 || g < 0 || g >= G) return DRS_ERR_ARG;
   cudaStream_t st = (cudaStream_t)stream;
-  k_shard_header<<<1, 1, 0, st>>>(totals, G, g, idx + make_index_desc(Mg).aoff);
+  const IndexDesc d = make_index_desc(Mg);
+  k_shard_header<<<1, 1, 0, st>>>(totals, G, g, idx + d.aoff, d.kt >= 2 ? 1 : 0);
   if (cudaGetLastError() != cudaSuccess) return DRS_ERR_LAUNCH;
   return launch_table_levels_from_aux(Mg, idx, st);
 }

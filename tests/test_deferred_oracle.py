@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 
-@pytest.mark.parametrize("M", [1, 2, 16, 17, 8447, 8448, 8449, 32 * 8448 + 3, 200_003])
+@pytest.mark.parametrize("M", [1, 2, 16, 17, 8447, 8448, 8449, 32 * 8448 + 3, 200_003, 262_144, 262_145, 600_001])
 def test_deferred_twin_equals_two_pass_twin(orc, M):
     rng = np.random.default_rng(M)
     w = np.exp(3.0 * rng.standard_normal(M))
@@ -22,9 +22,11 @@ def test_deferred_twin_equals_two_pass_twin(orc, M):
     assert st == st2 == 0
     np.testing.assert_array_equal(W, W2)
     ns = orc.search_entries(M)
-    np.testing.assert_array_equal(idx[:ns], orc.build_index(W2)[:ns])
+    ref_idx, l1 = orc.index_l1_local(V, orc.build_index(W2))
+    np.testing.assert_array_equal(idx[:ns], ref_idx[:ns])
     T = idx[ns]
-    assert idx[ns + 1] == 1.0 and T > 0
+    assert idx[ns + 1] == (5.0 if l1 else 1.0) and T > 0
+    assert l1 == (M > 16 * 16384)  # level 1 in-tile once the top guide sits above it
     P = idx[ns + 4:].reshape(-1, 2)
     assert P.shape[0] == -(-M // 8448) and P[0, 0] == 0.0 and P[0, 1] == 0.0
     t = np.arange(M) // 8448
