@@ -129,19 +129,23 @@ __device__ __forceinline__ void stage_to_w(double* sw, int len, int64_t j0, int6
   }
 }
 
-// W[j] at the end of a 16-entry block (j = 16 m + 15, or M - 1): level 1 of
-// the index holds these values -- W itself, or (TAB_L1) the in-tile value,
-// turned into W with the header and the tile pair (loaded after the header:
-// only such tables pay the second round trip); a table without an index is
-// direct
+// W[j] at the end of a 16-entry block (j = 16 m + 15, or M - 1): a direct
+// table's value itself (often already in L2: the neighbouring tile's copy);
+// for a deferred table level 1 of the index, which holds W there -- or
+// (TAB_L1) the in-tile value, turned into W with the tile pair.  The value
+// and the header are loaded together; only a deferred table pays the second
+// round trip.  A table without an index is direct.
 __device__ __forceinline__ double block_end_w(const double* __restrict__ W, const double* __restrict__ idx,
                                               const double* __restrict__ aux, int64_t M, int64_t j) {
-  if (!(idx && M > FANOUT)) return __ldg(W + j);
-  const double v = __ldg(idx + j / FANOUT);  // level 1 sits at offset 0
+  const double v = __ldg(W + j);
+  if (!aux) return v;
   const double2 h = __ldg(reinterpret_cast<const double2*>(aux));
-  if (!((int)h.y & TAB_L1)) return v;
+  const int mode = (int)h.y;
+  if (mode == 0) return v;
+  const double l1v = __ldg(idx + j / FANOUT);  // level 1 sits at offset 0 (a deferred table has M > 16 here or idx)
+  if (!(mode & TAB_L1)) return (M > FANOUT) ? l1v : tab_w(load_aux(aux), __ldg(reinterpret_cast<const double2*>(aux + TAB_HDR) + j / TABLE_TILE), v, j == M - 1);
   const TabAux ta = load_aux(aux);
-  return tab_w(ta, __ldg(ta.P + j / TABLE_TILE), v, j == M - 1);
+  return tab_w(ta, __ldg(ta.P + j / TABLE_TILE), l1v, j == M - 1);
 }
 
 constexpr int MT_THREADS = 256;
@@ -179,16 +183,19 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
     if (len_even > 0) bulk_g2s(sw, W + j0, (uint32_t)len_even * 8u, &bar);
   }
   if (threadIdx.x == 64 && (len & 1)) sw[len - 1] = W[j0 + len - 1];
-  if (threadIdx.x >= 96 && threadIdx.x < 99) {
-    // the table header and a deferred table's tile pairs around j0 (unused,
-    // all zero, for a direct table), loaded beside the u-run searches
-    if (threadIdx.x == 96) {
-      s_hdr = aux ? __ldg(reinterpret_cast<const double2*>(aux)) : make_double2(1.0, 0.0);
-      s_hdr2 = aux ? __ldg(reinterpret_cast<const double2*>(aux) + 1) : make_double2(0.0, 1.0);
-    }
-    else if (aux) s_pair[threadIdx.x - 97] = __ldg(reinterpret_cast<const double2*>(aux + TAB_HDR) +
-                                                   min(j0 / TABLE_TILE + (threadIdx.x - 97), table_tiles(M) - 1));
+  if (threadIdx.x == 96) {
+    // the table header and, for a deferred table, its tile pairs around j0:
+    // loaded beside the u-run searches (a direct table loads the header only)
+    const double2 h = aux ? __ldg(reinterpret_cast<const double2*>(aux)) : make_double2(1.0, 0.0);
+    s_hdr = h;
+    s_hdr2 = aux ? __ldg(reinterpret_cast<const double2*>(aux) + 1) : make_double2(0.0, 1.0);
     s_probe = 0;
+    if (h.y != 0.0) {
+      const double2* P = reinterpret_cast<const double2*>(aux + TAB_HDR);
+      const int64_t t0 = j0 / TABLE_TILE, tl = table_tiles(M) - 1;
+      s_pair[0] = __ldg(P + t0);
+      s_pair[1] = __ldg(P + (t0 + 1 < tl ? t0 + 1 : tl));
+    }
   }
   if (warp == 0) {  // tile edges are block ends (tw is a multiple of 16): level 1 holds W there
     const int64_t v = (t == 0) ? 0 : warp_count_le(U, N, block_end_w(W, idx, aux, M, j0 - 1));
@@ -219,30 +226,39 @@ __global__ void __launch_bounds__(MT_THREADS, 8) k_merge_tiles(const double* __r
   }
   // short u-runs (or no room for a u chunk: paths == 0): a bisection per u
   if (!paths || ie - ib <= 2 * MT_THREADS) {
-    for (int seg = 0; seg < 2; ++seg) {
-      const int64_t r0 = seg ? sk1 : ib, r1 = seg ? ie : sk0;
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += MT_THREADS) {
-        const double x = __ldg(U + i);
-        int lo = 0, hi = len - 1;
-        if (*(volatile int*)&s_probe) {
-          const int jb = (int)((j0 / TABLE_TILE + 1) * TABLE_TILE - j0);
+    if (s_probe) {  // a deferred table, few u's: W formed at each probe (CTA-uniform branch)
+      const int jb = (int)((j0 / TABLE_TILE + 1) * TABLE_TILE - j0);
+      const bool shard = ((int)s_hdr.y & TAB_SHARD) != 0, pin = s_hdr2.y != 0.0;
+      for (int seg = 0; seg < 2; ++seg) {
+        const int64_t r0 = seg ? sk1 : ib, r1 = seg ? ie : sk0;
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += MT_THREADS) {
+          const double x = __ldg(U + i);
+          int lo = 0, hi = len - 1;
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             const double2 cd = s_pair[mid < jb ? 0 : 1];
             double S = __dadd_rn(cd.x, __dadd_rn(cd.y, sw[mid]));
-            if ((int)s_hdr.y & TAB_SHARD) S = __dadd_rn(s_hdr2.x, S);  // a shard of a W-sharded table
-            const double v = (j0 + mid == M - 1 && s_hdr2.y != 0.0) ? 1.0 : fmin(__ddiv_rn(S, s_hdr.x), 1.0);
+            if (shard) S = __dadd_rn(s_hdr2.x, S);  // a shard of a W-sharded table
+            const double v = (j0 + mid == M - 1 && pin) ? 1.0 : fmin(__ddiv_rn(S, s_hdr.x), 1.0);
             if (v < x) lo = mid + 1;
             else hi = mid;
           }
-        } else {
+          out[i] = j0 + lo;
+        }
+      }
+    } else {
+      for (int seg = 0; seg < 2; ++seg) {
+        const int64_t r0 = seg ? sk1 : ib, r1 = seg ? ie : sk0;
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += MT_THREADS) {
+          const double x = __ldg(U + i);
+          int lo = 0, hi = len - 1;
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (sw[mid] < x) lo = mid + 1;
             else hi = mid;
           }
+          out[i] = j0 + lo;
         }
-        out[i] = j0 + lo;
       }
     }
     pdl_trigger();

@@ -68,6 +68,27 @@ def test_c5_full_size_bit_exact(drs, orc, c5):
     print({k: (v["flips"], v["near_boundary_4ulp"], v["near_boundary_drift"]) for k, v in reports.items()})
 
 
+def test_c5_deferred_equals_two_pass(drs, c5):
+    """Config 5 at full size through both kinds of table: the single-pass
+    (deferred, level 1 in-tile) table's W, formed on the device, is the
+    two-pass table's W bit for bit over all 2^30 entries, and every sampler
+    returns the same 2^24 indices from both (test_c5_full_size_bit_exact pins
+    the deferred one against the oracle)."""
+    w, c = c5
+    N = c["N"]
+    wd = torch.from_numpy(w).cuda()
+    td = drs.build_weight_table(wd)
+    tt = drs.build_weight_table(wd, deferred=False)
+    del wd
+    assert td.deferred and not tt.deferred
+    assert torch.equal(td.device_cum, tt.device_values)
+    for fn, kw in ((drs.dac_sampler, {}), (drs.dac_sampler, {"mode": "merge"}), (drs.ccf_sampler, {}),
+                   (drs.binary_sampler, {})):
+        a = fn(td, N, drs.RngStream(c["useed"]), device=True, **kw)
+        b = fn(tt, N, drs.RngStream(c["useed"]), device=True, **kw)
+        assert torch.equal(a, b), (fn.__name__, kw)
+
+
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3"])
 def test_boundary_report_device_mode(drs, cfg):
     """The north star's proximity report at c1-c3: device W and U vs the
