@@ -43,7 +43,7 @@ c = bench.CONFIGS[cfg]
 L = _lib.lib()
 TUS = {"scan": ["pass1", "chain", "pass2", "finalize", "table_local", "table_levels", "k6", "k7"],
        "match": ["k0", "k1", "k2", "k3", "merge_tiles", "merge_heavy", "k6", "k7"],
-       "": ["k0", "k1", "k2", "k3", "k4", "k5", "k6", "k7"]}
+       "": ["k0", "k1", "k2", "k3", "k4", "k5", "finish", "k7"]}
 for tu in TUS:
     sfx = f"_{tu}" if tu else ""
     getattr(L, f"dr_debug_phase_times{sfx}").argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -77,8 +77,8 @@ for tu, names in TUS.items():
     getattr(L, f"dr_debug_phase_times{'_' + tu if tu else ''}")(buf.ctypes.data, buf.size)
     t = buf.reshape(8, 65536, 4).astype(np.float64)
     for k in range(8):
-        if tu == "" :
-            continue  # the fused kernels stamp with the older per-phase layout (scripts/phase_times.py)
+        if tu == "" and k != 6:
+            continue  # k_dac_fused stamps with the older per-phase layout (scripts/phase_times.py); k_finish_search is k = 6
         ent = t[k, :, 0]
         live = ent > 0
         if live.any():
