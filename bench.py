@@ -281,7 +281,10 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         # the dominant kernel: the fused sampler kernel when the step is that one
         # launch, else the search over a fixed U
         kernel_step = eager_step if (fused and args.sampler == "dac") else match
-        e2e_step = lambda: sampler(table, N, stream, **kw)  # noqa: E731
+        # the reference's call, dac_sampler(table, n, stream) (its timed region,
+        # bench.py:193-204): host result, no uniforms output
+        e2e_kw = {"mode": args.mode} if args.sampler == "dac" else {}
+        e2e_step = lambda: sampler(table, N, stream, **e2e_kw)  # noqa: E731
         e2e_h2d, e2e_d2h = 0, 8 * N
 
     # ---- warm-up

@@ -67,6 +67,7 @@ _PROTOS = {
     "dr_match_binary": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p]),
     "dr_sample_binary": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _i64, _c_void_p, _c_void_p]),
     "dr_sample_dac": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
+    "dr_sample_dac_sync": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
     "dr_sample_dac_gather": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i64, _i64, _i64, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
     "dr_sample_dac_from": (_int, [_c_void_p, _c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _i32, _c_void_p, _size, _c_void_p]),
     "dr_sample_ccf": (_int, [_c_void_p, _c_void_p, _i64, _u64, _u64, _u64, _c_void_p, _i64, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),

@@ -21,6 +21,9 @@
 // advanced on the device, so the launch can be captured in a CUDA graph
 // and replayed with fresh draws each time.
 #include <cooperative_groups.h>
+#include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "drs_common.cuh"
 
@@ -821,10 +824,72 @@ struct GatherSpec {
 int launch_gather_rows(const double* states, int64_t K, int64_t d, const int64_t* idx, int64_t N, int64_t divisor,
                        double* out, int32_t* status, cudaStream_t st);
 
+// The fused kernel's launch.  A cooperative launch costs ~7 us of host time
+// per call (the co-residency check); the same launch as the one kernel node
+// of a graph, instantiated once per (device, stream, grid) with the
+// cooperative attribute and re-parameterised per call
+// (cudaGraphExecKernelNodeSetParams), costs less host time.  A stream being
+// captured (the caller's own CUDA graph) takes the plain cooperative launch.
+struct FusedGraph {
+  int dev;
+  cudaStream_t st;
+  unsigned grid;
+  cudaGraphExec_t ex;
+  cudaGraphNode_t node;
+};
+
+static cudaError_t launch_fused(const FusedArgs& a, unsigned grid, cudaStream_t st, bool graph) {
+  static const bool use_graph = getenv("DRS_NO_GRAPH") == nullptr;
+  static std::mutex mu;
+  static std::vector<FusedGraph> cache;
+  static bool broken = false;
+  void* args[] = {(void*)&a};
+  if (graph && use_graph && !broken) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    int dev = 0;
+    if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone &&
+        cudaGetDevice(&dev) == cudaSuccess) {
+      cudaKernelNodeParams p = {};
+      p.func = (void*)k_dac_fused;
+      p.gridDim = dim3(grid);
+      p.blockDim = dim3(THREADS);
+      p.sharedMemBytes = (unsigned)(SIDX_CAP * 8);
+      p.kernelParams = args;
+      std::lock_guard<std::mutex> lk(mu);
+      FusedGraph* f = nullptr;
+      for (auto& c : cache)
+        if (c.dev == dev && c.st == st && c.grid == grid) f = &c;
+      if (!f) {
+        cudaGraph_t g = nullptr;
+        FusedGraph n{dev, st, grid, nullptr, nullptr};
+        cudaLaunchAttributeValue v = {};
+        v.cooperative = 1;
+        bool ok = cudaGraphCreate(&g, 0) == cudaSuccess && cudaGraphAddKernelNode(&n.node, g, nullptr, 0, &p) == cudaSuccess &&
+                  cudaGraphKernelNodeSetAttribute(n.node, cudaLaunchAttributeCooperative, &v) == cudaSuccess &&
+                  cudaGraphInstantiate(&n.ex, g, 0) == cudaSuccess;
+        if (!ok) {
+          cudaGetLastError();
+          broken = true;  // the plain cooperative launch from now on
+        } else {
+          cache.push_back(n);
+          f = &cache.back();
+        }
+      }
+      if (f) {
+        if (cudaGraphExecKernelNodeSetParams(f->ex, f->node, &p) == cudaSuccess) return cudaGraphLaunch(f->ex, st);
+        cudaGetLastError();
+        broken = true;
+      }
+    }
+  }
+  return cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3(grid), dim3(THREADS), args, (size_t)SIDX_CAP * 8, st);
+}
+
 static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
                            uint64_t offset, uint64_t* offset_dev, const double* raw, int64_t N,
                            double* U, int64_t* out, int32_t* status, int32_t mode, void* ws,
-                           size_t ws_bytes, cudaStream_t st, const GatherSpec* g = nullptr) {
+                           size_t ws_bytes, cudaStream_t st, const GatherSpec* g = nullptr,
+                           bool graph = false) {
   if (M < 1 || N < 1 || !W || !out || !status || !ws || !U) return DRS_ERR_ARG;
   if (mode != DRS_DAC_AUTO && mode != DRS_DAC_MERGE && mode != DRS_DAC_SEARCH) return DRS_ERR_MODE;
   if ((uintptr_t)W & 31) return DRS_ERR_ALIGN;
@@ -841,10 +906,7 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
     a.states = g ? g->states : nullptr; a.gout = g ? g->gout : nullptr;
     a.K = g ? g->K : 0; a.gd = g ? g->gd : 0; a.divisor = g ? g->divisor : 1;
     a.gd_vec2 = g && (g->gd % 2 == 0) && ((((uintptr_t)g->states) | ((uintptr_t)g->gout)) & 15) == 0;
-    void* args[] = {&a};
-    const cudaError_t e = cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3((unsigned)nt), dim3(THREADS),
-                                                      args, (size_t)SIDX_CAP * 8, st);
-    return e == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+    return launch_fused(a, (unsigned)nt, st, graph) == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
   }
   const int rc = raw ? sorted_uniforms_from_launch(raw, N, U, status, ws, ws_bytes, st)
                      : sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
@@ -882,6 +944,15 @@ int dr_sample_dac(const double* W, const double* idx, int64_t M, uint64_t k0, ui
                   int32_t* status, int32_t mode, void* ws, size_t ws_bytes, void* stream) {
   return sample_dac_impl(W, idx, M, k0, k1, offset, offset_dev, nullptr, N, U, out, status, mode, ws,
                          ws_bytes, (cudaStream_t)stream);
+}
+
+int dr_sample_dac_sync(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
+                       uint64_t offset, uint64_t* offset_dev, int64_t N, double* U, int64_t* out,
+                       int32_t* status, int32_t mode, void* ws, size_t ws_bytes, void* stream) {
+  const int rc = sample_dac_impl(W, idx, M, k0, k1, offset, offset_dev, nullptr, N, U, out, status, mode, ws,
+                                 ws_bytes, (cudaStream_t)stream, nullptr, true);
+  if (rc) return rc;
+  return cudaStreamSynchronize((cudaStream_t)stream) == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
 }
 
 int dr_sample_dac_gather(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,

@@ -19,6 +19,7 @@ from the table, the uniforms and the indices (``dr_op_counts``).
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -283,7 +284,54 @@ def _draw_uniforms(stream, n: int) -> torch.Tensor:
     return to_device_f64(stream.uniforms(n))[0]
 
 
+# The per-call host path of the common call (a host RngStream, no out= /
+# uniforms_out= / stats=): the per-(device, stream, n) scratch pointers are
+# looked up once, and one call into the CPython extension _drshost launches
+# dr_sample_dac / dr_sample_ccf and, for a host result, synchronises the
+# stream (drs_host.c).  Without the extension the ctypes path below runs the
+# same kernels.
+try:
+    from . import _drshost as _hc
+except ImportError:  # not built: the ctypes path
+    _hc = None
+_hc_bound = False
+_plans: dict[tuple[int, int, int], tuple[int, int, int, int]] = {}
+_raw_stream = _lib._raw_stream
+
+
+def _fast_sorted(kind: str, table: WeightTable, n: int, stream: RngStream, device: bool, mode: str):
+    global _hc_bound
+    dev = torch.cuda.current_device()
+    s = _raw_stream(dev)
+    plan = _plans.get((dev, s, n))
+    if plan is None:
+        L = _lib.lib()
+        if not _hc_bound:
+            addr = lambda f: ctypes.cast(f, ctypes.c_void_p).value  # noqa: E731
+            _hc.bind(addr(L.dr_sample_dac), addr(L.dr_sample_dac_sync), addr(L.dr_sample_ccf),
+                     addr(L.dr_stream_synchronize))
+            _hc_bound = True
+        ws, wsb = _lib.workspace(_lib.workspace_bytes(_lib.OP_SORTED, n), s)
+        # buffers superseded later stay allocated (_retired / _lib._ws_retired), so a plan stays valid
+        plan = (_scratch_uniforms(n, s).data_ptr(), _status_buf(s).data_ptr(), ws, wsb)
+        _plans[(dev, s, n)] = plan
+    k0, k1 = stream._key
+    off = stream._take(n + 1)
+    out = empty_i64(n) if device else host_result_i64(n)
+    idx = table._idx
+    rc = _hc.sorted_sample(0 if kind == "dac" else 1, table._W.data_ptr(), 0 if idx is None else idx.data_ptr(),
+                           table.size, k0, k1, off, n, plan[0], out.data_ptr(), plan[1], _lib.DAC_MODES[mode],
+                           plan[2], plan[3], s, 0 if device else 1)
+    if rc:
+        _lib.check(rc, f"dr_sample_{kind}")
+    return out if device else out.numpy()
+
+
 def _sorted_sampler(kind, table, n, stream, stats, device, mode="auto", out=None, U=None):
+    if _hc is not None and out is None and U is None and stats is None and type(stream) is RngStream:
+        n = int(n)
+        if n > 0:
+            return _fast_sorted(kind, table, n, stream, device, mode)
     n = int(n)
     if n < 0:
         raise ValueError("n must be >= 0")
