@@ -254,10 +254,10 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
   for (int blk = lane; blk < nblk; blk += 2 * LANES) {  // two blocks per lane in flight
     const int blk2 = blk + LANES;
     const U64x4 v = philox_block(k0, k1, b0 + (uint64_t)blk);
-    const U64x4 v2 = philox_block(k0, k1, b0 + (uint64_t)blk2);
     words[4 * blk + 0] = v.w0; words[4 * blk + 1] = v.w1;
     words[4 * blk + 2] = v.w2; words[4 * blk + 3] = v.w3;
-    if (blk2 < nblk) {
+    if (blk2 < nblk) {  // a warp whose lanes all lie past the last block skips the second block
+      const U64x4 v2 = philox_block(k0, k1, b0 + (uint64_t)blk2);
       words[4 * blk2 + 0] = v2.w0; words[4 * blk2 + 1] = v2.w1;
       words[4 * blk2 + 2] = v2.w2; words[4 * blk2 + 3] = v2.w3;
     }
@@ -271,8 +271,10 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
   for (int w = 0; w < NW; ++w) {
     const int e0 = 64 * w + 2 * lane;
     const bool v0 = e0 < ne, v1 = e0 + 1 < ne;
-    const double l0 = neglog(u01(words[a0 + (v0 ? e0 : 0)]));
-    const double l1 = neglog(u01(words[a0 + (v1 ? e0 + 1 : 0)]));
+    // rows before the last are full (64 (NW - 1) < ne); in the last one a log
+    // no lane needs is not issued at all (N_f = 256: one spacing in that row)
+    const double l0 = (w < NW - 1 || v0) ? neglog(u01(words[a0 + (v0 ? e0 : 0)])) : 0.0;
+    const double l1 = (w < NW - 1 || v1) ? neglog(u01(words[a0 + (v1 ? e0 + 1 : 0)])) : 0.0;
     const double z0 = v0 ? l0 : 0.0, z1 = v1 ? l1 : 0.0;
     const unsigned long long m0 = (v0 && !(z0 > 0.0)) ? 0ull
                                   : (v0 ? (unsigned long long)__double_as_longlong(z0) : 0x7FF0000000000000ULL);
@@ -320,8 +322,12 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
     const double Q = rows[w * (LANES + 1) + lane];
-    u0[w] = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc0[w])), A);
-    u1[w] = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc1[w])), A);
+    if (w < NW - 1 || 64 * w < Nf) {  // the last row may hold only the (n+1)-th spacing, never stored
+      u0[w] = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc0[w])), A);
+      u1[w] = __ddiv_rn(__dadd_rn(R[w], __dadd_rn(Q, sc1[w])), A);
+    } else {
+      u0[w] = u1[w] = 2.0;
+    }
   }
 #pragma unroll
   for (int w = 0; w < NW; ++w) {
