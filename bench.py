@@ -573,8 +573,10 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         "data": "synthetic (seeded numpy weights, SURVEY.md 8(d)); Philox draws",
         "config": {
             "workload": cfg, **{k: v for k, v in c.items()}, "sampler": args.sampler, "mode": args.mode,
-            "table": args.table,
-            "timed": "sorted uniforms + search per step, table resident (reference bench.py:193-204)",
+            "table": "per-filter tables formed in shared memory (never stored)" if cfg == "c4" else args.table,
+            "timed": ("per step: every filter's table scan + sorted uniforms + search, raw weights resident "
+                      "(the reference's per-filter loop, cdf.py:59-89 + samplers.py:262-266)") if cfg == "c4"
+            else "sorted uniforms + search per step, table resident (reference bench.py:193-204)",
             "l2": "flushed (256 MiB write) before every timed step; steps timed individually",
             "parallelism": ("shard-W" if cfg == "c5" else ("shard-filters" if cfg == "c4" else "replicas")) + f"x{world}",
         },
