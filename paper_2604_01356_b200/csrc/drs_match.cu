@@ -475,7 +475,9 @@ int launch_merge(const double* W, const double* idx, int64_t M, const double* U,
 __global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ idx, IndexDesc d) {
   extern __shared__ __align__(128) double sL[];
   __shared__ __align__(8) uint64_t bar;
+  STAMPK(6, 0);
   pdl_wait();
+  STAMPK(6, 1);
   pdl_trigger();
   const int64_t nk = d.n[d.kt];
   const uint32_t bytes = (uint32_t)(cdiv(nk, FANOUT) * FANOUT * 8);  // the level is padded to whole nodes
@@ -502,6 +504,7 @@ __global__ void __launch_bounds__(256) k_build_top_guide(double* __restrict__ id
     else hi = m;
   }
   G[b] = (int32_t)lo;
+  STAMPK(6, 3);
 }
 
 int launch_top_guide(int64_t M, double* idx, cudaStream_t st) {

@@ -16,6 +16,7 @@
 // uniform pass generates each draw once, writes the in-tile sums in pass 1 and
 // turns them into U in pass 2 (24 bytes per u).
 #include <algorithm>
+#include <cstdlib>
 
 #include "drs_common.cuh"
 
@@ -426,7 +427,8 @@ __global__ void __launch_bounds__(THREADS) k_table_pass2(const double* __restric
 // w once and writes the table once: 16 bytes per entry instead of 24.
 template <bool LOGW>
 __global__ void __launch_bounds__(THREADS) k_table_local(const double* __restrict__ w, int64_t n, ScanWS ws,
-                                                         double* __restrict__ L, double* __restrict__ lvl1) {
+                                                         double* __restrict__ L, double* __restrict__ lvl1,
+                                                         double* __restrict__ lvl2) {
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ FoldSmem fs;
@@ -478,6 +480,17 @@ __global__ void __launch_bounds__(THREADS) k_table_local(const double* __restric
     for (int64_t m = j0 / FANOUT + threadIdx.x; m < (jl + 1) / FANOUT; m += THREADS)
       lvl1[m] = sm[(m + 1) * FANOUT - 1 - j0];
     if (jl == n - 1 && (n % FANOUT) && threadIdx.x == 0) lvl1[(n - 1) / FANOUT] = sm[len - 1];
+  }
+  if (lvl2) {
+    // the sources of level 2 (the in-tile value at every 256-entry block end,
+    // 33 per tile), left in level 2's own slots: the kernel after the chain
+    // turns them into W in place with coalesced accesses instead of gathering
+    // one sector per 128-byte line of level 1
+    constexpr int64_t B2 = (int64_t)FANOUT * FANOUT;
+    static_assert(TS % B2 == 0, "level-2 blocks never straddle table tiles");
+    const int64_t jl = j0 + len - 1;
+    for (int64_t m = j0 / B2 + threadIdx.x; m < (jl + 1) / B2; m += THREADS) lvl2[m] = sm[(m + 1) * B2 - 1 - j0];
+    if (jl == n - 1 && (n % B2) && threadIdx.x == 0) lvl2[(n - 1) / B2] = sm[len - 1];
   }
   if (threadIdx.x == 0 && len_even > 0) bulk_commit_wait();
   STAMPK(4, 3);
@@ -543,7 +556,8 @@ __global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, Sca
       const int64_t m = (m2 * FANOUT + FANOUT - 1 < n1 - 1) ? m2 * FANOUT + FANOUT - 1 : n1 - 1;
       const uint32_t tt = (uint32_t)m / BLOCKS_PER_TILE;
       const double2 cd = FROM_WS ? make_double2(ws.grp[tt / GROUP_TILES], ws.incl[tt]) : __ldg(P + tt);
-      const double sl = __dadd_rn(cd.x, __dadd_rn(cd.y, idx[m]));
+      // the source value: left in level 2's slot by k_table_local (FROM_WS), else level-1 entry m
+      const double sl = __dadd_rn(cd.x, __dadd_rn(cd.y, FROM_WS ? idx[d.off[2] + m2] : idx[m]));
       const double S = shard ? __dadd_rn(O, sl) : sl;
       const bool lastm = m == n1 - 1;
       const double v = (lastm && pin) ? 1.0 : fmin(div_rn(S, byT), 1.0);
@@ -586,6 +600,166 @@ __global__ void __launch_bounds__(256) k_table_levels(int64_t M, int64_t nt, Sca
       }
     }
   }
+}
+
+// The chain and the levels in ONE launch (dr_build_table_deferred, tables
+// whose level 1 stays in-tile and whose tile totals fit in shared memory:
+// 2^18 < M <= TAIL_MAX_TILES * 8448).  One 1024-thread CTA per SM; every CTA
+// folds the whole tile chain itself out of shared memory -- the nt totals are
+// L2-resident (k_table_local has just written them), thread g folds group g,
+// thread 0 the group totals: k_chain_groups' fold, bit for bit -- instead of
+// waiting for a one-CTA kernel to do it and write it back: the chain launch,
+// its drain and its round trip through the workspace leave the critical path.
+// Each thread loads the sources of its level-2 entries (the in-tile values
+// k_table_local left in level 2's slots) behind the totals, then forms W in
+// place and stores the levels above;
+// the CTA's slice of the tile pairs goes to the header from shared memory.
+// CTA 0 finishes what k_chain_groups (mode 0) finishes: T, the status word.
+constexpr int TAIL_THREADS = 1024;
+constexpr int64_t TAIL_MAX_TILES = 16384;  // (nt + nt / 32 + ng) * 8 bytes of shared memory: <= 140 KB
+constexpr int TAIL_PRE = 4;                // level-2 entries per thread loaded ahead of the fold
+
+__global__ void __launch_bounds__(TAIL_THREADS) k_table_tail(int64_t M, int64_t nt, ScanWS ws, double* __restrict__ idx,
+                                                             IndexDesc d, int32_t* status_out) {
+  extern __shared__ __align__(16) double tsm[];
+  STAMPK(5, 0);
+  pdl_wait();
+  STAMPK(5, 1);
+  pdl_trigger();
+  const int64_t ng = cdiv(nt, GROUP_TILES);
+  double* sa = tsm;                          // [nt + nt / 32 (+1)] tile totals -> D_t, one pad slot per group
+  double* sE = tsm + nt + nt / GROUP_TILES + 1;  // [ng] group totals -> C_g
+  const int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n1 = d.n[1], n2 = d.n[2];
+  // 1. stage the tile totals (eight loads per thread in flight), and behind
+  // them the sources of this thread's first level-2 entries
+  double pre[TAIL_PRE];
+  for (int64_t tb = threadIdx.x; tb < nt || tb == threadIdx.x; tb += 8 * TAIL_THREADS) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t t = tb + (int64_t)k * TAIL_THREADS;
+      v[k] = (t < nt) ? __ldcg(ws.agg + t) : 0.0;
+    }
+    if (tb == threadIdx.x) {
+#pragma unroll
+      for (int k = 0; k < TAIL_PRE; ++k) {
+        // an always-valid address (no select on the loaded value, which would wait for it here)
+        const int64_t m2 = (e0 + k * stride < n2) ? e0 + k * stride : n2 - 1;
+        pre[k] = __ldcg(idx + d.off[2] + m2);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t t = tb + (int64_t)k * TAIL_THREADS;
+      if (t < nt) sa[t + (t >> 5)] = v[k];
+    }
+  }
+  __syncthreads();
+  STAMPK(7, 0);
+  // 2. thread g folds group g (exclusive, left to right from 0.0)
+  static_assert(TAIL_MAX_TILES / GROUP_TILES <= TAIL_THREADS, "one thread per group");
+  if (threadIdx.x < ng) {
+    const int64_t g = threadIdx.x;
+    const int len = (int)(((g + 1) * GROUP_TILES < nt ? (g + 1) * GROUP_TILES : nt) - g * GROUP_TILES);
+    double* ga = sa + g * (GROUP_TILES + 1);
+    double D = 0.0;
+    int t = 0;
+    for (; t + 8 <= len; t += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = ga[t + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        ga[t + k] = D;
+        D = __dadd_rn(D, v[k]);
+      }
+    }
+    for (; t < len; ++t) {
+      const double v = ga[t];
+      ga[t] = D;
+      D = __dadd_rn(D, v);
+    }
+    sE[g] = D;
+  }
+  __syncthreads();
+  STAMPK(7, 1);
+  // 3. thread 0 folds the group totals (eight loads ahead of the adds)
+  __shared__ double s_T;
+  if (threadIdx.x == 0) {
+    double C = 0.0;
+    int64_t g = 0;
+    for (; g + 8 <= ng; g += 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = sE[g + k];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        sE[g + k] = C;
+        C = __dadd_rn(C, v[k]);
+      }
+    }
+    for (; g < ng; ++g) {
+      const double e = sE[g];
+      sE[g] = C;
+      C = __dadd_rn(C, e);
+    }
+    s_T = C;
+    if (blockIdx.x == 0) {
+      ws.hdr->total = C;
+      uint32_t st = ws.hdr->status;
+      if (C == 0.0) st |= DRS_ST_DEGENERATE;
+      if (!(C < dinf())) st |= DRS_ST_ACCUM_OVERFLOW;
+      if (status_out) *status_out = (int32_t)st;
+      ws.hdr->status = 0;
+    }
+  }
+  __syncthreads();
+  STAMPK(5, 2);
+  const double T = s_T;
+  // 4. the header, the tile pairs, the +inf padding of every level
+  double* aux = idx + d.aoff;
+  for (int64_t e = e0; e < nt; e += stride)
+    reinterpret_cast<double2*>(aux + TAB_HDR)[e] = make_double2(sE[e / GROUP_TILES], sa[e + (e >> 5)]);
+  if (e0 == 0) {
+    aux[0] = T;
+    aux[1] = (double)(TAB_DEFERRED | TAB_L1);
+    aux[2] = 0.0;
+    aux[3] = 1.0;
+  }
+  if (e0 < (int64_t)FANOUT * d.levels) {
+    const int k = 1 + (int)(e0 / FANOUT);
+    const int64_t p = d.n[k] + e0 % FANOUT;
+    if (p < cdiv(d.n[k], FANOUT) * FANOUT) idx[d.off[k] + p] = dinf();
+  }
+  STAMPK(7, 2);
+  // 5. level 2 and above: the W of level-1 entry m = 16 m2 + 15 (the last: n1 - 1)
+  const DivBy byT = div_by(T);
+  constexpr uint32_t BLOCKS_PER_TILE = (uint32_t)(TABLE_TILE / FANOUT);
+  int k = 0;
+  for (int64_t m2 = e0; m2 < n2; m2 += stride, ++k) {
+    const int64_t m = (m2 * FANOUT + FANOUT - 1 < n1 - 1) ? m2 * FANOUT + FANOUT - 1 : n1 - 1;
+    double l;
+    switch (k) {  // the first TAIL_PRE are in registers
+      case 0: l = pre[0]; break;
+      case 1: l = pre[1]; break;
+      case 2: l = pre[2]; break;
+      case 3: l = pre[3]; break;
+      default: l = __ldcg(idx + d.off[2] + m2); break;
+    }
+    static_assert(TAIL_PRE == 4, "the switch above names the preloaded entries");
+    const uint32_t tt = (uint32_t)m / BLOCKS_PER_TILE;
+    const double S = __dadd_rn(sE[tt / GROUP_TILES], __dadd_rn(sa[tt + (tt >> 5)], l));
+    const bool lastm = m == n1 - 1;
+    const double v = lastm ? 1.0 : fmin(div_rn(S, byT), 1.0);
+    idx[d.off[2] + m2] = v;
+    for (int kk = 3, sh = 8; kk <= d.levels; ++kk, sh += 4) {
+      if (!lastm && ((m + 1) & (((int64_t)1 << sh) - 1)) != 0) break;
+      idx[d.off[kk] + (m >> sh)] = v;
+    }
+  }
+  STAMPK(5, 3);
 }
 
 // a shard's scan (dr_shard_scan_deferred): the tile pairs from the chain's
@@ -822,13 +996,25 @@ static int build_deferred(const double* w, bool logw, int64_t M, double* L, doub
   const ScanWS s = carve(ws, ws_bytes);
   const int smem = THREADS * K_TABLE * 8;
   double* lvl1 = d.levels > 0 ? idx + d.off[1] : nullptr;
+  double* lvl2 = d.kt >= 2 ? idx + d.off[2] : nullptr;  // level 1 stays in-tile: level 2's sources
   if (logw) {
     const int64_t mb = cdiv(M, 256 * 8);
     const unsigned mgrid = (unsigned)(mb < nt ? (mb < 1 ? 1 : mb) : nt);  // partials fit in agg[nt]
     launch_pdl(k_max_logw, dim3(mgrid < 1184 ? mgrid : 1184), dim3(256), 0, st, w, M, s);
-    launch_pdl(k_table_local<true>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, L, lvl1);
+    launch_pdl(k_table_local<true>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, L, lvl1, lvl2);
   } else {
-    launch_pdl(k_table_local<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, L, lvl1);
+    launch_pdl(k_table_local<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w, M, s, L, lvl1, lvl2);
+  }
+  if (d.kt >= 2 && nt <= TAIL_MAX_TILES && !getenv("DRS_NO_TABLE_TAIL")) {
+    // the chain and the levels in one launch (k_table_tail), then the guide
+    static SmemLimit lim_t;
+    const size_t tsmem = (size_t)(nt + nt / GROUP_TILES + 1 + cdiv(nt, GROUP_TILES)) * 8;
+    lim_t.raise((const void*)k_table_tail, (size_t)(TAIL_MAX_TILES + TAIL_MAX_TILES / GROUP_TILES + 1 +
+                                                     TAIL_MAX_TILES / GROUP_TILES) * 8);
+    const int64_t tgrid = std::min<int64_t>(cdiv(std::max<int64_t>(d.n[2], nt), TAIL_THREADS), drs_sm_count());
+    launch_pdl(k_table_tail, dim3((unsigned)tgrid), dim3(TAIL_THREADS), tsmem, st, M, nt, s, idx, d, status);
+    if (launch_rc()) return DRS_ERR_LAUNCH;
+    return launch_top_guide(M, idx, st);
   }
   launch_chain(s, nt, 0, status, nullptr, st);
   int64_t work = nt;
@@ -1041,7 +1227,7 @@ int dr_shard_scan_deferred(const double* w_shard, int64_t Mg, double* V, double*
   cudaStream_t st = (cudaStream_t)stream;
   const int smem = THREADS * K_TABLE * 8;
   launch_pdl(k_table_local<false>, dim3((unsigned)nt), dim3(THREADS), smem, st, w_shard, Mg, s, V,
-             d.levels > 0 ? idx + d.off[1] : (double*)nullptr);
+             d.levels > 0 ? idx + d.off[1] : (double*)nullptr, (double*)nullptr);
   launch_chain(s, nt, 0, status, Tg, st);
   launch_pdl(k_table_pairs, dim3((unsigned)std::min<int64_t>(cdiv(nt, 256), 1184)), dim3(256), 0, st, nt, s,
              idx + d.aoff);

@@ -41,8 +41,8 @@ sampler = sys.argv[2] if len(sys.argv) > 2 else "dac"
 mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
 c = bench.CONFIGS[cfg]
 L = _lib.lib()
-TUS = {"scan": ["pass1", "chain", "pass2", "finalize", "table_local", "table_levels", "k6", "k7"],
-       "match": ["k0", "k1", "k2", "k3", "merge_tiles", "merge_heavy", "k6", "k7"],
+TUS = {"scan": ["pass1", "chain", "pass2", "finalize", "table_local", "table_levels", "k6", "tail_phases"],
+       "match": ["k0", "k1", "k2", "k3", "merge_tiles", "merge_heavy", "top_guide", "k7"],
        "": ["k0", "k1", "k2", "k3", "k4", "k5", "finish", "k7"]}
 for tu in TUS:
     sfx = f"_{tu}" if tu else ""

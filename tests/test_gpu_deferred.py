@@ -19,7 +19,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 EDGE_M = [1, 2, 15, 16, 17, 255, 256, 257, 8447, 8448, 8449, 32 * 8448, 32 * 8448 + 1, 3 * 8448 + 5,
-          (1 << 20) + 7]
+          (1 << 18), (1 << 18) + 1, 33 * 8448 + 255, (1 << 20) + 7, 1000 * 8448 + 77]
 
 
 def _weights(M, seed):
@@ -59,6 +59,21 @@ def test_deferred_arrays_bit_exact_vs_oracle(drs, orc, M):
     i2 = t2.device_index.cpu().numpy()
     np.testing.assert_array_equal(orc.index_l1_local(V, i2)[0][:ns], idx[:ns])
     np.testing.assert_array_equal(t2.device_index.cpu().numpy()[ns:], 0.0)  # direct header
+
+
+@pytest.mark.parametrize("M", [(1 << 18) + 1, 300000, 64 * 8448, (1 << 22) + 5, 4097 * 8448])
+def test_table_tail_equals_chain_and_levels(drs, M, monkeypatch):
+    """dr_build_table_deferred finishes tables of 2^18 < M <= 16384 tiles with ONE
+    launch after the pass (k_table_tail: every CTA folds the tile chain itself);
+    DRS_NO_TABLE_TAIL=1 selects the chain + levels kernels it replaces (larger
+    tables always use them).  Same association, same bytes."""
+    w = torch.from_numpy(_weights(M, M + 1)).cuda()
+    monkeypatch.delenv("DRS_NO_TABLE_TAIL", raising=False)
+    a = drs.build_weight_table(w)
+    monkeypatch.setenv("DRS_NO_TABLE_TAIL", "1")
+    b = drs.build_weight_table(w)
+    assert torch.equal(a.device_values.view(torch.int64), b.device_values.view(torch.int64))
+    assert torch.equal(a.device_index.view(torch.int64), b.device_index.view(torch.int64))
 
 
 @pytest.mark.parametrize("M", [17, 8449, 300_001, 256 * 8448 + 5])
