@@ -158,6 +158,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def cdiv_(a, b):
+    return -(-a // b)
+
+
 # ---------------------------------------------------------------- drs arm
 def run_drs(args, rank, world, local_rank, cfg=None, light=False):
     """One config on this rank; rank 0's JSON line.  ``light``: the timed
@@ -178,8 +182,15 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         if world > 1:
             dist.barrier()
 
+    flush_r = torch.zeros(256 << 20, dtype=torch.uint8, device=dev).view(torch.int32) if args.flush == "write+read" else None
+
     def l2_flush():
+        # a 256 MiB write evicts everything but leaves L2 full of its own dirty lines, which the
+        # timed kernel would then have to write back (~126 MB, ~19 us at the copy peak, charged to
+        # whatever runs next); the read sweep of a second buffer replaces them by clean lines
         flush.fill_(1)
+        if flush_r is not None:
+            torch.sum(flush_r)
 
     # ---- untimed setup (the reference builds its table untimed too)
     if cfg == "c4":
@@ -419,9 +430,10 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         del w_dev, Wb, ib
         table_build = {"ms": tbm, "GB/s": 16 * M_ / (tbm * 1e-3) / 1e9,
                        "frac": 16 * M_ / (tbm * 1e-3) / 1e9 / peak_hbm()[0],
-                       "algorithmic_bytes": 16 * M_, "launches": 4,
-                       "note": "single pass (dr_build_table_deferred): read w once, write the table once, "
-                               "+ level 1 of the index read and written (M/16 each); local, chain, levels, guide",
+                       "algorithmic_bytes": 16 * M_, "launches": 3 if 32 < cdiv_(M_, 8448) <= 16384 else 4,
+                       "note": "single pass (dr_build_table_deferred): read w once, write the table once "
+                               "(+ level 1 of the index, M/16); then the tile chain + the levels above 1 in one "
+                               "launch (k_table_tail; the chain and levels kernels for > 16384 tiles), then the guide",
                        "two_pass_ms": tb2,
                        "two_pass_note": "dr_build_table: pass 1 reads w, pass 2 reads w again and writes W",
                        "timed": "the C ABI on preallocated table buffers (CUDA events, L2 flushed)",
@@ -577,7 +589,10 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
             "timed": ("per step: every filter's table scan + sorted uniforms + search, raw weights resident "
                       "(the reference's per-filter loop, cdf.py:59-89 + samplers.py:262-266)") if cfg == "c4"
             else "sorted uniforms + search per step, table resident (reference bench.py:193-204)",
-            "l2": "flushed (256 MiB write) before every timed step; steps timed individually",
+            "l2": ("flushed (256 MiB write, then a 256 MiB read sweep of a second buffer so that no dirty "
+                   "flush lines are written back inside the timed region) before every timed step; steps timed "
+                   "individually") if args.flush == "write+read"
+            else "flushed (256 MiB write) before every timed step; steps timed individually",
             "parallelism": ("shard-W" if cfg == "c5" else ("shard-filters" if cfg == "c4" else "replicas")) + f"x{world}",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -809,6 +824,9 @@ def main():
                     help="gloo: functional check of the multi-rank flow only (never a perf number)")
     ap.add_argument("--no-parity", dest="parity", action="store_false",
                     help="skip the device-mode parity block (oracle checker, after the timed region)")
+    ap.add_argument("--flush", default="write", choices=["write", "write+read"],
+                    help="L2 flush before every timed step: a 256 MiB write, or that write followed by a "
+                         "256 MiB read sweep (no dirty flush lines left for the timed kernel to write back)")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager API calls instead of CUDA-graph replays")
     args = ap.parse_args()

@@ -390,7 +390,10 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   // 1. stage the top index levels in shared memory (TMA bulk copy) and
   // prefetch the next global levels into L2 (one slice per CTA): both overlap
   // steps 2-4, so the search finds them on chip instead of in HBM
-  const uint32_t sbytes = (uint32_t)(a.sl.count * 8);
+  // a.out == nullptr: the sorted uniforms alone (U written, no table touched):
+  // dr_sorted_uniforms and the merge samplers' uniforms in one launch
+  const bool search = a.out != nullptr;
+  const uint32_t sbytes = search ? (uint32_t)(a.sl.count * 8) : 0u;
   if (threadIdx.x == 0) {
     s_min = 0x7FF0000000000000ULL;
     s_flag = 0;
@@ -401,7 +404,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
     mbar_init(&bar, 1);
     mbar_expect_tx(&bar, sbytes);
     if (sbytes) bulk_g2s(sidx, a.idx + a.sl.base, sbytes, &bar);
-    const int64_t lvl = (a.sl.k_smem >= 2) ? a.sl.base - a.d.off[a.sl.k_smem - 1] : 0;  // doubles
+    const int64_t lvl = (search && a.sl.k_smem >= 2) ? a.sl.base - a.d.off[a.sl.k_smem - 1] : 0;  // doubles
     const int64_t cap = lvl < L2_PREFETCH_DOUBLES ? lvl : L2_PREFETCH_DOUBLES;
     const int64_t plo = a.sl.base - cap;
     const int64_t per = cdiv(cdiv(a.sl.base - plo, (int64_t)gridDim.x), 2) * 2;  // 16-byte multiples
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   }
   __syncthreads();
   STAMP(9);
-  if (threadIdx.x == THREADS - 32 && a.sl.hdr >= 0) {
+  if (search && threadIdx.x == THREADS - 32 && a.sl.hdr >= 0) {
     // a deferred table's tile pairs (a W line, or a level-1 node, needs its
     // tile's pair: 16 bytes per 8448 entries, 127 KB at M = 2^26) into L2, one
     // slice per CTA, while warp 0 folds the chain; the header came with the staged
@@ -582,23 +585,27 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
 
   // 5. search: K_UNIF sorted u's per thread, top index levels in shared memory
   STAMP(5);
-  mbar_wait(&bar, 0);
-  STAMP(6);
-  // the table header arrived with the staged levels (no global round trip here)
-  const TabAux ta = (a.sl.hdr >= 0) ? tab_aux_at(sidx + a.sl.hdr, a.idx + a.d.aoff)
-                                    : load_aux(a.idx ? a.idx + a.d.aoff : nullptr);
   int64_t r[K_UNIF];
-  search_k_sm(a.W, a.idx, sidx, a.d, a.sl, ta, u, r);
-  STAMP(7);
-
-  // 6. write back: one 16-byte store per lane when aligned, so a warp's
-  // stores cover whole lines (the destination may be pinned host memory)
-  if (K_UNIF == 2 && e0 + 2 <= n && (((uintptr_t)(a.out + e0)) & 15) == 0) {
-    *reinterpret_cast<longlong2*>(a.out + e0) = make_longlong2((long long)r[0], (long long)r[K_UNIF - 1]);
-  } else {
 #pragma unroll
-    for (int i = 0; i < K_UNIF; ++i)
-      if (e0 + i < n) a.out[e0 + i] = r[i];
+  for (int i = 0; i < K_UNIF; ++i) r[i] = 0;
+  if (search) {  // grid-uniform
+    mbar_wait(&bar, 0);
+    STAMP(6);
+    // the table header arrived with the staged levels (no global round trip here)
+    const TabAux ta = (a.sl.hdr >= 0) ? tab_aux_at(sidx + a.sl.hdr, a.idx + a.d.aoff)
+                                      : load_aux(a.idx ? a.idx + a.d.aoff : nullptr);
+    search_k_sm(a.W, a.idx, sidx, a.d, a.sl, ta, u, r);
+    STAMP(7);
+
+    // 6. write back: one 16-byte store per lane when aligned, so a warp's
+    // stores cover whole lines (the destination may be pinned host memory)
+    if (K_UNIF == 2 && e0 + 2 <= n && (((uintptr_t)(a.out + e0)) & 15) == 0) {
+      *reinterpret_cast<longlong2*>(a.out + e0) = make_longlong2((long long)r[0], (long long)r[K_UNIF - 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < K_UNIF; ++i)
+        if (e0 + i < n) a.out[e0 + i] = r[i];
+    }
   }
   if (a.U && !need) {
     if (e0 + K_UNIF <= n && vec_ok(a.U + e0)) {
@@ -609,7 +616,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
         if (e0 + i < n) a.U[e0 + i] = u[i];
     }
   }
-  if (a.gout) {
+  if (search && a.gout) {
     // the resampled particle states, straight from the indices in registers
     // (lane l holds rows 2l, 2l+1 of the warp's 64).  The host checked
     // (M - 1) / divisor < K, so every row exists.
@@ -838,7 +845,8 @@ struct FusedGraph {
   cudaGraphNode_t node;
 };
 
-static cudaError_t launch_fused(const FusedArgs& a, unsigned grid, cudaStream_t st, bool graph) {
+static cudaError_t launch_fused(const FusedArgs& a, unsigned grid, cudaStream_t st, bool graph,
+                                size_t smem = (size_t)SIDX_CAP * 8) {
   static const bool use_graph = getenv("DRS_NO_GRAPH") == nullptr;
   static std::mutex mu;
   static std::vector<FusedGraph> cache;
@@ -882,7 +890,30 @@ static cudaError_t launch_fused(const FusedArgs& a, unsigned grid, cudaStream_t 
       }
     }
   }
-  return cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3(grid), dim3(THREADS), args, (size_t)SIDX_CAP * 8, st);
+  return cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3(grid), dim3(THREADS), args, smem, st);
+}
+
+// The sorted uniforms alone as ONE cooperative launch (k_dac_fused without a
+// table: draws, -log, in-tile chain, counter exchange, every CTA folds the
+// tile chain, U = Z / Z[n], the repair behind grid barriers) when the n + 1
+// spacings fit a co-resident grid; the pass 1 / chain / pass 2 / finalize
+// pipeline otherwise.  U, the status word and the device stream advance are
+// bit-identical either way (tests/test_gpu_parity.py).
+int sorted_uniforms_auto(uint64_t k0, uint64_t k1, uint64_t offset, uint64_t* offset_dev, const double* raw,
+                         int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const int64_t nt = cdiv(n + 1, TS_U);
+  const bool fused_ok = getenv("DRS_NO_FUSED_UNIFORMS") == nullptr;  // the pipeline, for A/B and tests
+  if (fused_ok && n >= 1 && U && nt <= coop_capacity() && nt <= FUSED_MAX_TILES && nt <= ws_capacity_tiles(ws_bytes)) {
+    FusedArgs a = {};
+    a.sl.hdr = -1;
+    a.k0 = k0; a.k1 = k1; a.offset = offset; a.offset_dev = offset_dev; a.raw = raw;
+    a.n = n; a.U = U; a.out = nullptr; a.status = status;
+    a.ws = carve_ws(ws, ws_bytes);
+    a.divisor = 1;
+    return launch_fused(a, (unsigned)nt, st, false, 0) == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
+  }
+  return raw ? sorted_uniforms_from_launch(raw, n, U, status, ws, ws_bytes, st)
+             : sorted_uniforms_launch(k0, k1, offset, offset_dev, n, U, status, ws, ws_bytes, st);
 }
 
 static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64_t k0, uint64_t k1,
@@ -908,8 +939,7 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
     a.gd_vec2 = g && (g->gd % 2 == 0) && ((((uintptr_t)g->states) | ((uintptr_t)g->gout)) & 15) == 0;
     return launch_fused(a, (unsigned)nt, st, graph) == cudaSuccess ? DRS_OK : DRS_ERR_LAUNCH;
   }
-  const int rc = raw ? sorted_uniforms_from_launch(raw, N, U, status, ws, ws_bytes, st)
-                     : sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
+  const int rc = sorted_uniforms_auto(k0, k1, offset, offset_dev, raw, N, U, status, ws, ws_bytes, st);
   if (rc) return rc;
   const int rm = merge ? launch_merge(W, idx, M, U, N, out, st) : launch_index(W, idx, M, U, N, out, st);
   if (rm || !g) return rm;
@@ -973,7 +1003,7 @@ int dr_sample_ccf(const double* W, const double* idx, int64_t M, uint64_t k0, ui
   if (M < 1 || N < 1 || !W || !U || !out || !status || !ws) return DRS_ERR_ARG;
   if ((uintptr_t)W & 15) return DRS_ERR_ALIGN;
   cudaStream_t st = (cudaStream_t)stream;
-  int rc = sorted_uniforms_launch(k0, k1, offset, offset_dev, N, U, status, ws, ws_bytes, st);
+  int rc = sorted_uniforms_auto(k0, k1, offset, offset_dev, nullptr, N, U, status, ws, ws_bytes, st);
   if (rc) return rc;
   return launch_merge(W, idx, M, U, N, out, st);
 }

@@ -1076,6 +1076,10 @@ int launch_table_levels_from_aux(int64_t M, double* idx, cudaStream_t st) {
   return launch_top_guide(M, idx, st);
 }
 
+// one cooperative launch when the spacings fit a co-resident grid, else the pipeline above (drs_fused.cu)
+int sorted_uniforms_auto(uint64_t k0, uint64_t k1, uint64_t offset, uint64_t* offset_dev, const double* raw,
+                         int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace drs
 
 using namespace drs;
@@ -1246,14 +1250,13 @@ int dr_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t k, double* u,
 int dr_sorted_uniforms(uint64_t k0, uint64_t k1, uint64_t offset, int64_t n, double* U,
                        int32_t* status, void* ws, size_t ws_bytes, void* stream) {
   if (n < 1 || !U || !status || !ws) return DRS_ERR_ARG;
-  return sorted_uniforms_launch(k0, k1, offset, nullptr, n, U, status, ws, ws_bytes, (cudaStream_t)stream);
+  return sorted_uniforms_auto(k0, k1, offset, nullptr, nullptr, n, U, status, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int dr_sorted_uniforms_from(const double* raw, int64_t n, double* U, int32_t* status, void* ws,
                             size_t ws_bytes, void* stream) {
   if (n < 1 || !raw || !U || !status || !ws) return DRS_ERR_ARG;
-  ArraySpacings src{raw};
-  return sorted_impl(src, n, U, status, ws, ws_bytes, nullptr, (cudaStream_t)stream);
+  return sorted_uniforms_auto(0, 0, 0, nullptr, raw, n, U, status, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -217,6 +217,30 @@ def test_sorted_uniforms_sizes(drs, orc, n):
     assert U[0] > 0 and U[-1] < 1 and np.all(np.diff(U) > 0)
 
 
+@pytest.mark.parametrize("n", [1, 2, 1023, 1025, 4095, 70001])
+def test_sorted_uniforms_pipeline_small_n(drs, orc, golden, n, monkeypatch):
+    """n + 1 spacings that fit a co-resident grid take ONE cooperative launch
+    (k_dac_fused without a table); DRS_NO_FUSED_UNIFORMS=1 selects the pass 1 /
+    chain / pass 2 / finalize pipeline that larger n always use: same U, same
+    repair, same stream advance."""
+    k0, k1 = orc.key_of(n, (3,))
+    Uo, _ = orc.sorted_uniforms(k0, k1, 5, n)
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("DRS_NO_FUSED_UNIFORMS", env)
+        else:
+            monkeypatch.delenv("DRS_NO_FUSED_UNIFORMS", raising=False)
+        s = drs.RngStream(n, (3,))
+        s.uniforms(5)
+        np.testing.assert_array_equal(drs.sorted_uniforms(s, n), Uo)
+        assert s.draws == 5 + n + 1
+    monkeypatch.setenv("DRS_NO_FUSED_UNIFORMS", "1")
+    for i in range(int(golden["rp_count"])):  # the replayed collapse / repair cases through the pipeline
+        d = golden[f"rp_draws_{i}"]
+        U = drs.sorted_uniforms(ReplayStream(d), d.shape[0] - 1)
+        np.testing.assert_array_equal(U, orc.sorted_uniforms_from(d, d.shape[0] - 1)[0])
+
+
 def test_replay_and_repair_bit_exact(drs, orc, golden):
     for i in range(int(golden["rp_count"])):
         d = golden[f"rp_draws_{i}"]
