@@ -12,6 +12,8 @@
 //        blocks (search mode); AUTO picks merge when M <= tau*N.
 // All three return the unique lower bound: first j with W[j] >= u (W[j] < u
 // compared strictly, ties to the first of an equal run), clamped to M-1.
+#include <cstdlib>
+
 #include "drs_common.cuh"
 
 namespace drs {
@@ -448,12 +450,16 @@ int launch_merge(const double* W, const double* idx, int64_t M, const double* U,
   const int sms = drs_sm_count();
   // tiles of up to 4096 entries; smaller for small tables so that every SM
   // gets >= ~6 tiles to overlap
-  int tw = MT_TW;  // 8192 / 16384: c3 ccf 105.8 / 118.3 us against 104.8 (scripts/merge_tw_sweep.sh)
+  int tw = MT_TW;  // 8192 / 16384: c3 ccf 105.8 / 118.3 us against 104.8
   while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
-  // when a tile holds few u's on average (M >> N) the u chunk of the merge
-  // path is not allocated: the CTA is its W tile alone, so more tiles are in
-  // flight per SM; a tile that still holds a long run bisects every u
-  const int paths = (double)N * tw >= 64.0 * (double)M ? 1 : 0;
+  // the CTA is its W tile alone (no u chunk: more tiles in flight per SM) and
+  // every u bisects the staged tile;
+  // measured (scripts/paths_ab.py, profiles/r2/merge_paths/): the per-u bisection of the staged tile is
+  // never slower than the linear merge path, whatever the u's per tile (N = M included: no u chunk to
+  // stage, no barriers, more CTAs per SM), so the merge path runs only when DRS_MERGE_PATHS_MIN (average
+  // u's per tile from which it is used) asks for it
+  const char* pm = getenv("DRS_MERGE_PATHS_MIN");
+  const int paths = pm && (double)N * tw >= atof(pm) * (double)M ? 1 : 0;
   const size_t smem = (size_t)(tw + (paths ? 2 * MT_UC : 0)) * sizeof(double);
   launch_pdl(k_merge_tiles, dim3((unsigned)cdiv(M, tw)), dim3(MT_THREADS), smem, st, W, M, idx, aux, U, N, out, tw,
              paths);

@@ -92,11 +92,18 @@ def test_exact_mode_large_random(drs, orc):
     (1 << 20, 70_001, 0.97, 1),            # one weight holds 97% of the mass: one run spans the u's
     ((1 << 18) + 1, 300_000, 0.3, 20000),  # a heavy block spanning several tiles
 ])
-def test_merge_heavy_runs(drs, orc, M, N, frac, blk):
-    """Tiles whose u-run is longer than MT_HEAVY: the tile CTA merges the
+@pytest.mark.parametrize("paths_min", [None, "64"])
+def test_merge_heavy_runs(drs, orc, M, N, frac, blk, paths_min, monkeypatch):
+    """Tiles whose u-run is longer than MT_HEAVY: the tile CTA handles the
     ragged ends, k_merge_heavy the whole chunks inside; bit-exact against the
     oracle's lower bounds with exact boundaries inside the heavy block, for
-    CCF and DaC in merge mode, with ragged N."""
+    CCF and DaC in merge mode, with ragged N.  Both tile bodies: the per-u
+    bisection of the staged tile (the default: measured never slower) and the
+    linear merge path from 64 u's per tile (DRS_MERGE_PATHS_MIN=64)."""
+    if paths_min:
+        monkeypatch.setenv("DRS_MERGE_PATHS_MIN", paths_min)
+    else:
+        monkeypatch.delenv("DRS_MERGE_PATHS_MIN", raising=False)
     rng = np.random.default_rng(79)
     w = np.exp(rng.standard_normal(M))
     off = int(rng.integers(0, M - blk))
