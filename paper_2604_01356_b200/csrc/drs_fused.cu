@@ -927,7 +927,7 @@ static int sample_dac_impl(const double* W, const double* idx, int64_t M, uint64
   const IndexDesc d = make_index_desc(M);
   if (d.levels > 0 && !idx) return DRS_ERR_ARG;
   const int64_t nt = cdiv(N + 1, TS_U);
-  const bool merge = (mode == DRS_DAC_MERGE) || (mode == DRS_DAC_AUTO && M <= 16 * N);
+  const bool merge = (mode == DRS_DAC_MERGE) || (mode == DRS_DAC_AUTO && M <= (int64_t)DRS_DAC_TAU * N);
   if (!merge && nt <= coop_capacity() && nt <= FUSED_MAX_TILES && nt <= ws_capacity_tiles(ws_bytes)) {
     FusedArgs a;
     a.W = W; a.idx = idx; a.d = d; a.sl = plan_smem_levels(d);

@@ -20,7 +20,7 @@ namespace drs {
 
 IndexDesc make_index_desc(int64_t M);  // drs_scan.cu
 
-constexpr int64_t DAC_TAU = 16;
+constexpr int64_t DAC_TAU = DRS_DAC_TAU;  // drs_common.cuh
 
 static int launch_rc() {
   const cudaError_t e = cudaGetLastError();

@@ -166,7 +166,7 @@ def dac_match(u, table: WeightTable, stats: OpStats | None = None, check: bool =
 
     ``mode``: "merge" splits u by table tiles and merges each slice (reads
     all of W); "search" splits by index blocks and bisects per u (reads
-    O(N log(M/N)) lines); "auto" picks merge when M <= 16 N.
+    O(N log(M/N)) lines); "auto" picks merge when M <= 11 N (the measured crossover).
     """
     if mode not in _lib.DAC_MODES:
         raise ValueError(f"unknown mode {mode!r}")
