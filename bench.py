@@ -534,6 +534,24 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
                            "timed": "CUDA events, L2 flushed, device table/states/result"}
         del xs
 
+    # ---- the north star's recast beside the headline (c3 dac auto searches the index and touches
+    # ~9.5 MB; mode="merge" streams all of W through shared-memory tiles, so its algorithmic bytes are
+    # its physical bytes and its fraction is a roofline fraction): same call, same flush discipline
+    merge_recast = None
+    if not light and cfg == "c3" and args.sampler == "dac" and args.mode != "merge":
+        mr_stream = drs.RngStream(c["useed"], (rank, 14))
+        mr_step = lambda: drs.dac_sampler(table, N, mr_stream, device=True, out=out_buf, mode="merge")  # noqa: E731
+        for _ in range(3):
+            mr_step()
+        mr_ms = statistics.median(timed(mr_step, max(5, min(args.steps, 20))))
+        tm = ROOT / "profiles" / f"traffic_{cfg}_dac_merge.json"
+        mr_traffic = json.loads(tm.read_text()) if tm.exists() else {}
+        merge_recast = {"mode": "merge", "ms_per_step": mr_ms, "GB/s": alg_bytes / (mr_ms * 1e-3) / 1e9,
+                        "frac": alg_bytes / (mr_ms * 1e-3) / 1e9 / peak_hbm()[0],
+                        "kernel_ncu": mr_traffic or None,
+                        "timed": "one dac_sampler(mode='merge') call per step (uniforms + k_merge_tiles + the "
+                                 "long-run helper), CUDA events, L2 flushed"}
+
     # ---- end to end through the public API, host result (and host weights for c4)
     e2e = None
     if e2e_step is not None:
@@ -604,6 +622,7 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
         "table_build": table_build,
         "filter_step": filter_step,
         "resample_gather": resample_gather,
+        "merge_recast": merge_recast,
         "clocks": clk.summary(),
         "step_ms_min": min(step_ms), "step_ms_median": statistics.median(step_ms),
         "timing": "one public-API sampler call per step (device result), CUDA events on the launching stream",
