@@ -284,7 +284,6 @@ __global__ void __launch_bounds__(UW_FILTERS * LANES, 7) k_batched_uniforms_warp
     sc0[w] = z0;
     sc1[w] = __dadd_rn(z0, z1);
   }
-#pragma unroll
   // rounded down to the high word (see block_min_u64): only the exactness trigger uses it
   mn = (unsigned long long)__reduce_min_sync(FULL, (unsigned)(mn >> 32)) << 32;
   WSTAMP(3);
@@ -372,7 +371,7 @@ __global__ void __launch_bounds__(THREADS) k_resample_batched(const __grid_const
   __shared__ double s_A[MAX_TT];  // tile totals, written by every CTA of the cluster
   __shared__ int s_bad;
   __shared__ double s_cend[THREADS];  // S at each lane chunk's last entry
-  const int64_t Mf = a.Mf, Nf = a.Nf, ne = Nf + 1;
+  const int64_t Mf = a.Mf, Nf = a.Nf;
   const int r = (int)cluster_rank();
   const int64_t f = blockIdx.x / a.ntt;
   const int64_t j0 = (int64_t)r * TS_TABLE;  // first weight of this tile

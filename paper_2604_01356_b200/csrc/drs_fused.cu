@@ -547,25 +547,19 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
     __syncthreads();
     if (lane == 0)
       prev_lane = (warp > 0) ? s_last[warp - 1] : ((t == 0) ? 0.0 : __ddiv_rn(__dadd_rn(Cg, P), total));
-    bool site = false;
 #pragma unroll
     for (int i = 0; i < K_UNIF; ++i) {
       const int64_t e = e0 + i;
       if (e < n) {
         const double pv = (i == 0) ? prev_lane : u[i - 1];
         if (u[i] <= pv) {
-          site = true;
           const uint32_t slot = atomicAdd(&a.ws.hdr->nsites, 1u);
           if (slot < (uint32_t)SITE_CAP) a.ws.sites[slot] = (long long)e;
         }
-        if (e == n - 1 && u[i] >= 1.0) {
-          site = true;
-          atomicOr(&a.ws.hdr->top, 1u);
-        }
+        if (e == n - 1 && u[i] >= 1.0) atomicOr(&a.ws.hdr->top, 1u);
       }
       if (e < n) a.U[e] = u[i];  // U must be in memory for the repair
     }
-    (void)site;
     grid_barrier(bcount, bgen);
     const uint32_t nsites = *(volatile uint32_t*)&a.ws.hdr->nsites;
     const uint32_t top = *(volatile uint32_t*)&a.ws.hdr->top;

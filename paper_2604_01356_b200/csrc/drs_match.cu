@@ -451,7 +451,13 @@ int launch_merge(const double* W, const double* idx, int64_t M, const double* U,
   // tiles of up to 4096 entries; smaller for small tables so that every SM
   // gets >= ~6 tiles to overlap
   int tw = MT_TW;  // 8192 / 16384: c3 ccf 105.8 / 118.3 us against 104.8
+  // from ~512 u's per 4096-entry tile a CTA's serial work (a u load and a
+  // bisection per u, 256 at a time) outweighs its fixed cost (the two u-run
+  // searches): half-size tiles (N = M = 2^22: 151 -> 113 us, 2^24: 497 -> 378 us;
+  // profiles/r2/merge_paths/tile_width_sweep.txt)
+  if ((double)N * MT_TW >= 512.0 * (double)M) tw = MT_TW / 2;
   while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
+  if (const char* f = getenv("DRS_MERGE_TW")) tw = atoi(f);  // sweeps only (a power of two in [256, 4096])
   // the CTA is its W tile alone (no u chunk: more tiles in flight per SM) and
   // every u bisects the staged tile;
   // measured (scripts/paths_ab.py, profiles/r2/merge_paths/): the per-u bisection of the staged tile is
