@@ -587,6 +587,8 @@ def run_drs(args, rank, world, local_rank, cfg=None, light=False):
     tp = ROOT / "profiles" / f"traffic_{cfg}_{args.sampler}_{args.mode}.json"
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+        if world > 1 and cfg in ("c4", "c5"):
+            traffic = None  # captured on one GPU for the whole bank / table: not this rank's launch
     line = {
         "metric": METRIC if cfg == "c3" else f"weights-scanned GB/s + samples/sec, {cfg}",
         "value": value,
