@@ -20,6 +20,7 @@
 // The stream position may live in device memory (offset_dev) and is then
 // advanced on the device, so the launch can be captured in a CUDA graph
 // and replayed with fresh draws each time.
+#include <algorithm>
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <mutex>
@@ -369,7 +370,12 @@ struct FusedArgs {
   bool gd_vec2;  // rows as 16-byte pairs (gd even, both bases aligned)
 };
 
-__global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant__ FusedArgs a) {
+// SEARCH = false: the sorted uniforms alone (a.out == nullptr: no table touched, no
+// index stage).  Its own instantiation, because without the search and the gather
+// it needs a quarter of the registers: four CTAs per SM are co-resident, so the
+// single cooperative launch covers n + 1 <= 4 * 148 * 512 spacings.
+template <bool SEARCH>
+__global__ void __launch_bounds__(THREADS, SEARCH ? 1 : 4) k_dac_fused(const __grid_constant__ FusedArgs a) {
   extern __shared__ __align__(128) double sidx[];
   __shared__ __align__(8) uint64_t bar;
   __shared__ FoldSmem fs;
@@ -390,9 +396,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_dac_fused(const __grid_constant_
   // 1. stage the top index levels in shared memory (TMA bulk copy) and
   // prefetch the next global levels into L2 (one slice per CTA): both overlap
   // steps 2-4, so the search finds them on chip instead of in HBM
-  // a.out == nullptr: the sorted uniforms alone (U written, no table touched):
-  // dr_sorted_uniforms and the merge samplers' uniforms in one launch
-  const bool search = a.out != nullptr;
+  constexpr bool search = SEARCH;
   const uint32_t sbytes = search ? (uint32_t)(a.sl.count * 8) : 0u;
   if (threadIdx.x == 0) {
     s_min = 0x7FF0000000000000ULL;
@@ -803,8 +807,12 @@ __global__ void k_advance_offset(uint64_t* p, uint64_t by) { *p += by; }
 static int coop_capacity() {
   static SmemLimit lim;
   static OccupancyCache occ;
-  lim.raise((const void*)k_dac_fused, SIDX_CAP * 8);
-  return drs_sm_count() * occ.get((const void*)k_dac_fused, THREADS, SIDX_CAP * 8);
+  lim.raise((const void*)k_dac_fused<true>, SIDX_CAP * 8);
+  return drs_sm_count() * occ.get((const void*)k_dac_fused<true>, THREADS, SIDX_CAP * 8);
+}
+static int coop_capacity_uniforms() {  // the uniforms-only instantiation: no dynamic shared memory
+  static OccupancyCache occ;
+  return drs_sm_count() * occ.get((const void*)k_dac_fused<false>, THREADS, 0);
 }
 
 }  // namespace drs
@@ -852,7 +860,7 @@ static cudaError_t launch_fused(const FusedArgs& a, unsigned grid, cudaStream_t 
     if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone &&
         cudaGetDevice(&dev) == cudaSuccess) {
       cudaKernelNodeParams p = {};
-      p.func = (void*)k_dac_fused;
+      p.func = (void*)k_dac_fused<true>;
       p.gridDim = dim3(grid);
       p.blockDim = dim3(THREADS);
       p.sharedMemBytes = (unsigned)(SIDX_CAP * 8);
@@ -884,10 +892,11 @@ static cudaError_t launch_fused(const FusedArgs& a, unsigned grid, cudaStream_t 
       }
     }
   }
-  return cudaLaunchCooperativeKernel((void*)k_dac_fused, dim3(grid), dim3(THREADS), args, smem, st);
+  return cudaLaunchCooperativeKernel(smem ? (void*)k_dac_fused<true> : (void*)k_dac_fused<false>, dim3(grid),
+                                     dim3(THREADS), args, smem, st);
 }
 
-// The sorted uniforms alone as ONE cooperative launch (k_dac_fused without a
+// The sorted uniforms alone as ONE cooperative launch (k_dac_fused<false>, no
 // table: draws, -log, in-tile chain, counter exchange, every CTA folds the
 // tile chain, U = Z / Z[n], the repair behind grid barriers) when the n + 1
 // spacings fit a co-resident grid; the pass 1 / chain / pass 2 / finalize
@@ -897,7 +906,10 @@ int sorted_uniforms_auto(uint64_t k0, uint64_t k1, uint64_t offset, uint64_t* of
                          int64_t n, double* U, int32_t* status, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int64_t nt = cdiv(n + 1, TS_U);
   const bool fused_ok = getenv("DRS_NO_FUSED_UNIFORMS") == nullptr;  // the pipeline, for A/B and tests
-  if (fused_ok && n >= 1 && U && nt <= coop_capacity() && nt <= FUSED_MAX_TILES && nt <= ws_capacity_tiles(ws_bytes)) {
+  // up to three tiles per SM: measured (scripts/mid_n_probe.py, M = 2^26 dac search) 19.5 vs 22.5 us at
+  // n = 75,776, 21.2 vs 24.2 at 2^17, 29.7 vs 30.7 at 2^18; at the fourth CTA per SM (n ~ 3 10^5) the pipeline wins
+  const int64_t fused_cap = std::min<int64_t>(coop_capacity_uniforms(), 3 * (int64_t)drs_sm_count());
+  if (fused_ok && n >= 1 && U && nt <= fused_cap && nt <= FUSED_MAX_TILES && nt <= ws_capacity_tiles(ws_bytes)) {
     FusedArgs a = {};
     a.sl.hdr = -1;
     a.k0 = k0; a.k1 = k1; a.offset = offset; a.offset_dev = offset_dev; a.raw = raw;

@@ -213,7 +213,7 @@ def test_sorted_uniforms_bit_exact_vs_oracle(drs, orc, golden):
         assert np.abs(U - ref).max() <= 1e-13
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 1022, 1023, 1024, 1025, 4095, 70001, 1 << 20])
+@pytest.mark.parametrize("n", [1, 2, 3, 1022, 1023, 1024, 1025, 4095, 70001, 75775, 75776, 150000, 227327, 227328, 303104, 1 << 20])
 def test_sorted_uniforms_sizes(drs, orc, n):
     s = drs.RngStream(n, (3,))
     s.uniforms(5)  # non-multiple-of-4 draw offset
@@ -224,10 +224,11 @@ def test_sorted_uniforms_sizes(drs, orc, n):
     assert U[0] > 0 and U[-1] < 1 and np.all(np.diff(U) > 0)
 
 
-@pytest.mark.parametrize("n", [1, 2, 1023, 1025, 4095, 70001])
+@pytest.mark.parametrize("n", [1, 2, 1023, 1025, 4095, 70001, 150000, 227327])
 def test_sorted_uniforms_pipeline_small_n(drs, orc, golden, n, monkeypatch):
-    """n + 1 spacings that fit a co-resident grid take ONE cooperative launch
-    (k_dac_fused without a table); DRS_NO_FUSED_UNIFORMS=1 selects the pass 1 /
+    """n + 1 spacings that fit a co-resident grid (up to three 512-spacing tiles per SM: 227,328 on a
+    148-SM part) take ONE cooperative launch (k_dac_fused<false>: no table);
+    DRS_NO_FUSED_UNIFORMS=1 selects the pass 1 /
     chain / pass 2 / finalize pipeline that larger n always use: same U, same
     repair, same stream advance."""
     k0, k1 = orc.key_of(n, (3,))
