@@ -152,6 +152,7 @@ __device__ __forceinline__ double block_end_w(const double* __restrict__ W, cons
 
 constexpr int MT_THREADS = 256;
 constexpr int MT_TW = 4096;   // max W entries per tile (32 KB)
+constexpr int MT_TW3 = 3072;  // tiles of large tables with few u's each (24 KB: eight CTAs per SM)
 constexpr int MT_UC = 1024;   // u's staged per merge-path chunk (8 KB)
 constexpr int MT_HEAVY = 4 * MT_UC;  // a tile's u-run longer than this is spread over k_merge_heavy
 
@@ -456,6 +457,10 @@ int launch_merge(const double* W, const double* idx, int64_t M, const double* U,
   // searches): half-size tiles (N = M = 2^22: 151 -> 113 us, 2^24: 497 -> 378 us;
   // profiles/r2/merge_paths/tile_width_sweep.txt)
   if ((double)N * MT_TW >= 512.0 * (double)M) tw = MT_TW / 2;
+  // few u's per tile (M >> N) and a large table: 24 KB tiles, so that eight CTAs (not seven) fit an SM and
+  // more u-run searches are in flight -- c5 ccf 2.09 -> 1.88 ms, M = 2^26 N = 2^20 145 -> 133 us, c3 ccf
+  // unchanged; 2560 / 2816 / 3328 / 3584 measured too (tile_width_sweep.txt: not monotone, 3072 the best)
+  else if (cdiv(M, MT_TW3) >= 6 * (int64_t)sms) tw = MT_TW3;
   while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
   if (const char* f = getenv("DRS_MERGE_TW")) tw = atoi(f);  // sweeps only (a power of two in [256, 4096])
   // the CTA is its W tile alone (no u chunk: more tiles in flight per SM) and
