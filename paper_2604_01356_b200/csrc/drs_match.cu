@@ -460,7 +460,8 @@ int launch_merge(const double* W, const double* idx, int64_t M, const double* U,
   // few u's per tile (M >> N) and a large table: 24 KB tiles, so that eight CTAs (not seven) fit an SM and
   // more u-run searches are in flight -- c5 ccf 2.09 -> 1.88 ms, M = 2^26 N = 2^20 145 -> 133 us, c3 ccf
   // unchanged; 2560 / 2816 / 3328 / 3584 measured too (tile_width_sweep.txt: not monotone, 3072 the best)
-  else if (cdiv(M, MT_TW3) >= 6 * (int64_t)sms) tw = MT_TW3;
+  // (with fewer than ~16 u's per tile the searches are few and the 32 KB tiles stream best: c3, ncu 85 vs 90 us)
+  else if ((double)N * MT_TW >= 16.0 * (double)M && cdiv(M, MT_TW3) >= 6 * (int64_t)sms) tw = MT_TW3;
   while (tw > 256 && cdiv(M, tw) < 6 * (int64_t)sms) tw >>= 1;
   if (const char* f = getenv("DRS_MERGE_TW")) tw = atoi(f);  // sweeps only (a power of two in [256, 4096])
   // the CTA is its W tile alone (no u chunk: more tiles in flight per SM) and
